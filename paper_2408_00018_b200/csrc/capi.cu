@@ -1,0 +1,549 @@
+// capi.cu — the extern "C" boundary (include/parsa_b200.h) and the host
+// driver of the device engines.
+//
+// Host-side semantics restate the reference exactly where they are host
+// logic: schedule validation and the do-while ladder (sa_core.cpp:8-35),
+// start resolution (engines.cpp:36-41), the reduce_min tie-break
+// (engines.cpp:55-64), trace bookkeeping (engines.cpp:48-51,198) and the
+// reference's exception messages, mapped to psa_status codes.  Everything
+// that touches chains runs on the device; there is no CPU fallback.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "engine_host.h"
+#include "libm_glibc64.cuh"
+#include "parsa_b200.h"
+
+using psa::Cand;
+using psa::EngineArgs;
+using psa::EngineKernels;
+using psa::OutScalars;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct Failure {
+    psa_status code;
+    std::string msg;
+};
+
+[[noreturn]] void fail(psa_status code, const std::string& msg) { throw Failure{code, msg}; }
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) {
+        std::ostringstream m;
+        m << "parsa_b200: " << what << ": " << cudaGetErrorString(e);
+        fail(PSA_ERR_CUDA, m.str());
+    }
+}
+
+template <class Fn>
+psa_status guarded(Fn&& fn) {
+    try {
+        fn();
+        return PSA_OK;
+    } catch (const Failure& f) {
+        g_err = f.msg;
+        return f.code;
+    } catch (const std::bad_alloc&) {
+        g_err = "parsa_b200: host allocation failed";
+        return PSA_ERR_CUDA;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return PSA_ERR_CUDA;
+    }
+}
+
+// sa_core.cpp:8-15
+void validate_schedule(const psa_schedule& s) {
+    if (!(s.t0 > 0) || !(s.t_min > 0) || !(s.t_min < s.t0))
+        fail(PSA_ERR_INVALID_ARGUMENT, "schedule: need 0 < t_min < t0");
+    if (!(s.rho > 0) || !(s.rho < 1)) fail(PSA_ERR_INVALID_ARGUMENT, "schedule: need rho in (0,1)");
+    if (s.sweep_length < 1) fail(PSA_ERR_INVALID_ARGUMENT, "schedule: need sweep_length >= 1");
+}
+
+// sa_core.cpp:17-27: repeated multiplication, not pow
+std::vector<double> ladder_of(const psa_schedule& s) {
+    validate_schedule(s);
+    std::vector<double> t;
+    double v = s.t0;
+    do {
+        t.push_back(v);
+        v *= s.rho;
+    } while (v > s.t_min);
+    return t;
+}
+
+uint64_t expected_evals(const psa_schedule& s, int n_chains, const char* who) {
+    if (n_chains < 1) fail(PSA_ERR_INVALID_ARGUMENT, std::string(who) + ": need n_chains >= 1");
+    const uint64_t levels = ladder_of(s).size();
+    return static_cast<uint64_t>(n_chains) * (1 + static_cast<uint64_t>(s.sweep_length) * levels);
+}
+
+void require_dim(int expected, int got, const char* what) {
+    if (expected != got) {
+        std::ostringstream m;
+        m << what << ": expected dimension " << expected << ", got " << got;
+        fail(PSA_ERR_INVALID_ARGUMENT, m.str());
+    }
+}
+
+void check_objective(const psa_objective* f) {
+    if (!f) fail(PSA_ERR_INVALID_ARGUMENT, "parsa_b200: null objective");
+    if (f->family < 0 || f->family >= PSA_FN_COUNT) {
+        std::ostringstream m;
+        m << "parsa_b200: no device implementation for objective '" << (f->id ? f->id : "?")
+          << "' (family " << f->family << ")";
+        fail(PSA_ERR_INVALID_ARGUMENT, m.str());
+    }
+    if (f->dim < 1 || !f->lower || !f->upper)
+        fail(PSA_ERR_INVALID_ARGUMENT, "parsa_b200: objective needs dim >= 1 and a box");
+    const int fam = f->family;
+    // formulas that read a fixed coordinate count (objectives.cpp:43-114,232-284)
+    int need = 0;
+    if (fam == PSA_FN_BRANIN || fam == PSA_FN_DEKKERS_AARTS || fam == PSA_FN_EASOM ||
+        fam == PSA_FN_GOLDSTEIN_PRICE || fam == PSA_FN_HIMMELBLAU || fam == PSA_FN_SIX_HUMP_CAMEL)
+        need = 2;
+    if (fam == PSA_FN_SHEKEL5 || fam == PSA_FN_SHEKEL7 || fam == PSA_FN_SHEKEL10) need = 4;
+    if (need && f->dim < need) fail(PSA_ERR_INVALID_ARGUMENT, "parsa_b200: dimension too small for family");
+    if ((fam == PSA_FN_MOD_LANGERMAN || fam == PSA_FN_SHEKEL_FOXHOLES) && f->dim > 10)
+        fail(PSA_ERR_INVALID_ARGUMENT, "parsa_b200: Langerman/Foxholes data has 10 columns");
+}
+
+// engines.cpp:36-41 + BoxDomain::center (objectives.cpp:484-488) + contains (:490-496)
+std::vector<double> resolve_start(const psa_objective* f, const psa_engine_config* cfg) {
+    const int n = f->dim;
+    std::vector<double> s(n);
+    if (cfg->start_point && cfg->start_point_len > 0) {
+        require_dim(n, cfg->start_point_len, "contains");
+        s.assign(cfg->start_point, cfg->start_point + cfg->start_point_len);
+    } else {
+        for (int k = 0; k < n; ++k) s[k] = 0.5 * (f->lower[k] + f->upper[k]);
+    }
+    for (int k = 0; k < n; ++k)
+        if (s[k] < f->lower[k] || s[k] > f->upper[k])
+            fail(PSA_ERR_INVALID_ARGUMENT, std::string("infeasible start point for ") + (f->id ? f->id : ""));
+    return s;
+}
+
+int device_count_sm100() {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    int ok = 0;
+    for (int d = 0; d < n; ++d) {
+        cudaDeviceProp p;
+        if (cudaGetDeviceProperties(&p, d) == cudaSuccess && p.major == 10) ++ok;
+    }
+    return ok;
+}
+
+void require_device() {
+    if (device_count_sm100() == 0)
+        fail(PSA_ERR_NO_DEVICE, "parsa_b200: no sm_100 CUDA device available (there is no CPU fallback)");
+}
+
+template <class T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    void alloc(size_t count) {
+        free();
+        n = count;
+        if (count) cuda_check(cudaMalloc(&p, sizeof(T) * count), "cudaMalloc");
+    }
+    void free() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    ~DevBuf() { free(); }
+};
+
+} // namespace
+
+struct psa_plan {
+    int engine = 2; // 1 async, 2 sync
+    int n = 0, levels = 0, N = 0, precision = 0, family = 0;
+    int32_t chains_local = 0;
+    uint32_t chain_begin = 0, chains_total = 0;
+    int random_start = 0;
+    std::vector<double> temps;
+    EngineKernels ks{};
+    int block = 128, grid = 0;
+    size_t smem = 0;
+    EngineArgs args{};
+    DevBuf<double> d_lower, d_width, d_start, d_temps, d_trace, d_bestx, d_xbest, d_winner_f;
+    DevBuf<int32_t> d_winner;
+    DevBuf<uint32_t> d_masks;
+    DevBuf<Cand> d_cand, d_cand_start, d_trace_cand;
+    DevBuf<OutScalars> d_out;
+    uint64_t expected_evals = 0, expected_draws = 0;
+};
+
+namespace {
+
+void plan_build(psa_plan* p, const psa_objective* f, const psa_engine_config* cfg, int engine,
+                int32_t chain_begin, int32_t chain_end) {
+    const char* who = engine == 1 ? "run_asynchronous" : "run_synchronous";
+    validate_schedule(cfg->schedule); // engines.cpp:133
+    if (cfg->n_chains < 1) fail(PSA_ERR_INVALID_ARGUMENT, std::string(who) + ": need n_chains >= 1");
+    check_objective(f);
+    p->temps = ladder_of(cfg->schedule);
+    const std::vector<double> start = resolve_start(f, cfg);
+    require_device();
+    if (chain_begin < 0 || chain_end > cfg->n_chains || chain_begin >= chain_end)
+        fail(PSA_ERR_INVALID_ARGUMENT, "parsa_b200: invalid chain shard");
+
+    p->engine = engine;
+    p->n = f->dim;
+    p->levels = static_cast<int>(p->temps.size());
+    p->N = cfg->schedule.sweep_length;
+    p->precision = cfg->precision == PSA_F32 ? PSA_F32 : PSA_F64;
+    p->family = f->family;
+    p->chain_begin = static_cast<uint32_t>(chain_begin);
+    p->chains_local = chain_end - chain_begin;
+    p->chains_total = static_cast<uint32_t>(cfg->n_chains);
+    p->random_start = cfg->start_mode == PSA_RANDOM_PER_CHAIN;
+    p->ks = psa::engine_kernels(p->precision, p->family);
+
+    const int n = p->n;
+    std::vector<double> width(n);
+    for (int k = 0; k < n; ++k) width[k] = f->upper[k] - f->lower[k]; // BoxDomain::width
+    bool uniform = true;
+    for (int k = 1; k < n; ++k)
+        if (f->lower[k] != f->lower[0] || width[k] != width[0]) uniform = false;
+
+    // block size: the largest of 128/64/32 whose state fits in shared memory
+    int dev = 0;
+    cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+    cudaDeviceProp prop;
+    cuda_check(cudaGetDeviceProperties(&prop, dev), "cudaGetDeviceProperties");
+    const size_t smem_cap = prop.sharedMemPerBlockOptin;
+    auto smem_of = [&](int B) { return engine == 1 ? p->ks.smem_v1(n, B) : p->ks.smem_v2(n, B); };
+    int B = 128;
+    while (B > 32 && smem_of(B) > smem_cap) B /= 2;
+    if (smem_of(B) > smem_cap)
+        fail(PSA_ERR_INVALID_ARGUMENT, "parsa_b200: dimension too large for the shared-memory chain state");
+    p->block = B;
+    p->smem = smem_of(B);
+    const void* kern = engine == 1 ? p->ks.v1 : p->ks.v2;
+    cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(p->smem)),
+               "cudaFuncSetAttribute");
+    int per_sm = 0;
+    cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, B, p->smem), "occupancy");
+    if (per_sm < 1) fail(PSA_ERR_CUDA, "parsa_b200: engine kernel cannot be resident");
+    const long long need = (static_cast<long long>(p->chains_local) + B - 1) / B;
+    p->grid = static_cast<int>(std::min<long long>(need, static_cast<long long>(per_sm) * prop.multiProcessorCount));
+
+    // device buffers
+    p->d_lower.alloc(n);
+    p->d_width.alloc(n);
+    p->d_start.alloc(n);
+    p->d_temps.alloc(p->levels);
+    p->d_trace.alloc(p->levels);
+    p->d_bestx.alloc(n);
+    p->d_out.alloc(1);
+    cuda_check(cudaMemcpy(p->d_lower.p, f->lower, sizeof(double) * n, cudaMemcpyHostToDevice), "H2D");
+    cuda_check(cudaMemcpy(p->d_width.p, width.data(), sizeof(double) * n, cudaMemcpyHostToDevice), "H2D");
+    cuda_check(cudaMemcpy(p->d_start.p, start.data(), sizeof(double) * n, cudaMemcpyHostToDevice), "H2D");
+    cuda_check(cudaMemcpy(p->d_temps.p, p->temps.data(), sizeof(double) * p->levels, cudaMemcpyHostToDevice), "H2D");
+    const size_t W = (p->N + 31) / 32;
+    if (engine == 2) {
+        p->d_masks.alloc(2 * W * static_cast<size_t>(p->chains_local));
+        p->d_cand.alloc(2 * static_cast<size_t>(p->grid));
+        p->d_cand_start.alloc(p->grid);
+        p->d_winner.alloc(p->levels);
+        p->d_winner_f.alloc(p->levels);
+    } else {
+        p->d_cand.alloc(p->grid);
+        p->d_trace_cand.alloc(static_cast<size_t>(p->levels) * p->grid);
+        p->d_xbest.alloc(static_cast<size_t>(p->grid) * B * n);
+    }
+
+    EngineArgs& a = p->args;
+    a.n = n;
+    a.family = p->family;
+    a.N = p->N;
+    a.levels = p->levels;
+    a.uniform_box = uniform;
+    a.random_start = p->random_start;
+    a.lo0 = f->lower[0];
+    a.w0 = width[0];
+    a.lower = p->d_lower.p;
+    a.width = p->d_width.p;
+    a.start = p->d_start.p;
+    a.temps = p->d_temps.p;
+    a.keys = psa::make_keys(cfg->seed);
+    a.chains_local = static_cast<size_t>(p->chains_local);
+    a.chain_begin = p->chain_begin;
+    a.chains_total = p->chains_total;
+    a.masks = p->d_masks.p;
+    a.cand = p->d_cand.p;
+    a.cand_start = p->d_cand_start.p;
+    a.trace_cand = p->d_trace_cand.p;
+    a.trace_best = p->d_trace.p;
+    a.best_x = p->d_bestx.p;
+    a.xbest = p->d_xbest.p;
+    a.level_winner = p->d_winner.p;
+    a.level_winner_f = p->d_winner_f.p;
+    a.out_scalars = p->d_out.p;
+
+    // engines.cpp:48-51 / sa_core.cpp:29-35
+    p->expected_evals = static_cast<uint64_t>(p->chains_local) *
+                        (1 + static_cast<uint64_t>(p->N) * static_cast<uint64_t>(p->levels));
+    p->expected_draws = 3ull * static_cast<uint64_t>(p->N) * p->levels * p->chains_local +
+                        (p->random_start ? static_cast<uint64_t>(n) * p->chains_local : 0);
+}
+
+void plan_launch(psa_plan* p, cudaStream_t s) {
+    cuda_check(cudaMemsetAsync(p->d_out.p, 0, sizeof(OutScalars), s), "memset");
+    void* params[] = {&p->args};
+    if (p->engine == 2) {
+        cuda_check(cudaLaunchCooperativeKernel(p->ks.v2, dim3(p->grid), dim3(p->block), params, p->smem, s),
+                   "launch v2_kernel");
+    } else {
+        cuda_check(cudaLaunchKernel(p->ks.v1, dim3(p->grid), dim3(p->block), params, p->smem, s),
+                   "launch v1_kernel");
+        int blocks = p->grid;
+        void* fparams[] = {&p->args, &blocks};
+        cuda_check(cudaLaunchKernel(psa::v1_finalize_kernel(), dim3(1), dim3(256), fparams, 0, s),
+                   "launch v1_finalize");
+    }
+}
+
+void plan_fetch(psa_plan* p, cudaStream_t s, psa_run_result* out) {
+    OutScalars o;
+    std::vector<double> trace(p->levels);
+    cuda_check(cudaMemcpyAsync(&o, p->d_out.p, sizeof(o), cudaMemcpyDeviceToHost, s), "D2H");
+    cuda_check(cudaMemcpyAsync(trace.data(), p->d_trace.p, sizeof(double) * p->levels, cudaMemcpyDeviceToHost, s), "D2H");
+    if (out->best_x)
+        cuda_check(cudaMemcpyAsync(out->best_x, p->d_bestx.p, sizeof(double) * p->n, cudaMemcpyDeviceToHost, s), "D2H");
+    cuda_check(cudaStreamSynchronize(s), "engine run");
+    // accounting cross-check (harness.cpp:148-155): the device counted every trial
+    if (o.evaluations != p->expected_evals || o.rng_draws != p->expected_draws) {
+        std::ostringstream m;
+        m << "evaluation count mismatch: engine reported " << o.evaluations << ", expected "
+          << p->expected_evals;
+        fail(PSA_ERR_LOGIC, m.str());
+    }
+    out->best_f = o.best_f;
+    out->winning_chain = o.best_chain;
+    out->evaluations = o.evaluations;
+    out->rng_draws = o.rng_draws;
+    out->has_phases = 0;
+    out->trace_len = p->levels;
+    for (int l = 0; l < p->levels && l < out->trace_capacity; ++l) {
+        out->trace[l].level = l;
+        out->trace[l].reserved = 0;
+        out->trace[l].cumulative_evals =
+            static_cast<uint64_t>(p->chains_local) * (1 + static_cast<uint64_t>(p->N) * (l + 1));
+        out->trace[l].best_f = trace[l];
+    }
+}
+
+psa_status run_engine(const psa_objective* f, const psa_engine_config* cfg, int engine,
+                      psa_run_result* out) {
+    return guarded([&] {
+        const auto t0 = std::chrono::steady_clock::now();
+        if (!out) fail(PSA_ERR_INVALID_ARGUMENT, "parsa_b200: null result");
+        psa_plan p;
+        plan_build(&p, f, cfg, engine, 0, cfg ? cfg->n_chains : 0);
+        cudaStream_t s;
+        cuda_check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
+        try {
+            plan_launch(&p, s);
+            plan_fetch(&p, s, out);
+        } catch (...) {
+            cudaStreamDestroy(s);
+            throw;
+        }
+        cudaStreamDestroy(s);
+        out->wall_time_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    });
+}
+
+} // namespace
+
+extern "C" {
+
+int32_t psa_abi_version(void) { return PSA_ABI_VERSION; }
+const char* psa_last_error(void) { return g_err.c_str(); }
+int32_t psa_device_count(void) { return device_count_sm100(); }
+
+psa_status psa_schedule_validate(const psa_schedule* s) {
+    return guarded([&] { validate_schedule(*s); });
+}
+
+psa_status psa_ladder(const psa_schedule* s, double* temps, int32_t capacity, int32_t* levels) {
+    return guarded([&] {
+        const auto t = ladder_of(*s);
+        if (levels) *levels = static_cast<int32_t>(t.size());
+        if (temps)
+            for (size_t i = 0; i < t.size() && static_cast<int32_t>(i) < capacity; ++i) temps[i] = t[i];
+    });
+}
+
+psa_status psa_expected_evaluations(const psa_schedule* s, int32_t n_chains, uint64_t* out) {
+    return guarded([&] { *out = expected_evals(*s, n_chains, "expected_evaluations"); });
+}
+
+psa_status psa_reduce_min(const double* f, const int32_t* chain, int32_t count, int32_t* pos) {
+    return guarded([&] {
+        if (count < 1) fail(PSA_ERR_INVALID_ARGUMENT, "reduce_min: empty candidate list");
+        int32_t best = 0;
+        for (int32_t i = 0; i < count; ++i)
+            if (f[i] < f[best] || (f[i] == f[best] && chain[i] < chain[best])) best = i;
+        *pos = best;
+    });
+}
+
+psa_status psa_run_synchronous(const psa_objective* f, const psa_engine_config* cfg, psa_run_result* out) {
+    return run_engine(f, cfg, 2, out);
+}
+
+psa_status psa_run_asynchronous(const psa_objective* f, const psa_engine_config* cfg, psa_run_result* out) {
+    return run_engine(f, cfg, 1, out);
+}
+
+psa_status psa_run_sequential(const psa_objective* f, const psa_engine_config* cfg, psa_run_result* out) {
+    if (cfg && cfg->n_chains != 1) {
+        g_err = "run_sequential: requires n_chains == 1";
+        return PSA_ERR_INVALID_ARGUMENT;
+    }
+    return run_engine(f, cfg, 1, out);
+}
+
+psa_status psa_nelder_mead_minimize(const psa_objective*, const double*, const psa_nm_config*, psa_nm_result*) {
+    g_err = "parsa_b200: nelder_mead_minimize is not available in this build";
+    return PSA_ERR_LOGIC;
+}
+
+psa_status psa_hybrid_run(const psa_objective*, const psa_engine_config*, const psa_schedule*,
+                          const psa_nm_config*, psa_run_result*) {
+    g_err = "parsa_b200: hybrid_run is not available in this build";
+    return PSA_ERR_LOGIC;
+}
+
+psa_status psa_plan_create(const psa_objective* f, const psa_engine_config* cfg, int32_t engine,
+                           int32_t chain_begin, int32_t chain_end, psa_plan** out) {
+    return guarded([&] {
+        if (engine != 1 && engine != 2) fail(PSA_ERR_INVALID_ARGUMENT, "parsa_b200: engine must be 1 or 2");
+        auto* p = new psa_plan;
+        try {
+            plan_build(p, f, cfg, engine, chain_begin, chain_end);
+        } catch (...) {
+            delete p;
+            throw;
+        }
+        *out = p;
+    });
+}
+
+psa_status psa_plan_launch(psa_plan* p, void* stream) {
+    return guarded([&] { plan_launch(p, static_cast<cudaStream_t>(stream)); });
+}
+
+psa_status psa_plan_fetch(psa_plan* p, void* stream, psa_run_result* out) {
+    return guarded([&] { plan_fetch(p, static_cast<cudaStream_t>(stream), out); });
+}
+
+psa_status psa_plan_info(const psa_plan* p, int32_t* levels, int32_t* chains, int32_t* launches) {
+    return guarded([&] {
+        if (levels) *levels = p->levels;
+        if (chains) *chains = p->chains_local;
+        if (launches) *launches = p->engine == 2 ? 1 : 2;
+    });
+}
+
+psa_status psa_plan_level_detail(const psa_plan* p, int32_t* winners, double* winner_f, int32_t capacity) {
+    return guarded([&] {
+        if (p->engine != 2) fail(PSA_ERR_INVALID_ARGUMENT, "parsa_b200: level detail needs the synchronous engine");
+        const int m = std::min(capacity, p->levels);
+        if (winners) cuda_check(cudaMemcpy(winners, p->d_winner.p, sizeof(int32_t) * m, cudaMemcpyDeviceToHost), "D2H");
+        if (winner_f) cuda_check(cudaMemcpy(winner_f, p->d_winner_f.p, sizeof(double) * m, cudaMemcpyDeviceToHost), "D2H");
+    });
+}
+
+psa_status psa_plan_destroy(psa_plan* p) {
+    delete p;
+    return PSA_OK;
+}
+
+psa_status psa_device_uniforms(uint64_t seed, uint32_t chain, uint32_t level, uint64_t first, int32_t count,
+                               double* out) {
+    return guarded([&] {
+        require_device();
+        DevBuf<double> d;
+        d.alloc(count);
+        int c = count;
+        void* params[] = {&seed, &chain, &level, &first, &c, &d.p};
+        cuda_check(cudaLaunchKernel(psa::probe_uniforms_kernel(), dim3((count + 255) / 256), dim3(256), params, 0, 0),
+                   "probe_uniforms");
+        cuda_check(cudaMemcpy(out, d.p, sizeof(double) * count, cudaMemcpyDeviceToHost), "D2H");
+    });
+}
+
+psa_status psa_device_philox(const uint32_t* ctr, const uint32_t* key, int32_t count, uint32_t* out) {
+    return guarded([&] {
+        require_device();
+        DevBuf<uint32_t> dc, dout;
+        dc.alloc(4 * static_cast<size_t>(count));
+        dout.alloc(4 * static_cast<size_t>(count));
+        cuda_check(cudaMemcpy(dc.p, ctr, sizeof(uint32_t) * 4 * count, cudaMemcpyHostToDevice), "H2D");
+        uint32_t k0 = key[0], k1 = key[1];
+        int c = count;
+        const uint32_t* cp = dc.p;
+        void* params[] = {&cp, &k0, &k1, &c, &dout.p};
+        cuda_check(cudaLaunchKernel(psa::probe_philox_kernel(), dim3((count + 255) / 256), dim3(256), params, 0, 0),
+                   "probe_philox");
+        cuda_check(cudaMemcpy(out, dout.p, sizeof(uint32_t) * 4 * count, cudaMemcpyDeviceToHost), "D2H");
+    });
+}
+
+psa_status psa_device_evaluate(const psa_objective* f, int32_t precision, const double* x, int32_t count,
+                               double* out) {
+    return guarded([&] {
+        check_objective(f);
+        require_device();
+        const int n = f->dim;
+        const EngineKernels ks = psa::engine_kernels(precision == PSA_F32 ? PSA_F32 : PSA_F64, f->family);
+        int B = 64;
+        while (B > 1 && ks.smem_eval(n, B) > 160 * 1024) B /= 2;
+        const size_t smem = ks.smem_eval(n, B);
+        cuda_check(cudaFuncSetAttribute(ks.eval, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
+                   "cudaFuncSetAttribute");
+        DevBuf<double> dx, dout;
+        dx.alloc(static_cast<size_t>(count) * n);
+        dout.alloc(count);
+        cuda_check(cudaMemcpy(dx.p, x, sizeof(double) * count * n, cudaMemcpyHostToDevice), "H2D");
+        EngineArgs a{};
+        a.n = n;
+        a.family = f->family;
+        int c = count;
+        const double* xp = dx.p;
+        void* params[] = {&a, &xp, &c, &dout.p};
+        cuda_check(cudaLaunchKernel(ks.eval, dim3((count + B - 1) / B), dim3(B), params, smem, 0), "probe_evaluate");
+        cuda_check(cudaMemcpy(out, dout.p, sizeof(double) * count, cudaMemcpyDeviceToHost), "D2H");
+    });
+}
+
+float psa_libm_sinf(float x) { return psa::libm::sinf(x); }
+float psa_libm_cosf(float x) { return psa::libm::cosf(x); }
+float psa_libm_expf(float x) { return psa::libm::expf(x); }
+double psa_libm_sin(double x) { return psa::libm::sin(x); }
+double psa_libm_cos(double x) { return psa::libm::cos(x); }
+double psa_libm_exp(double x) { return psa::libm::exp(x); }
+
+} // extern "C"

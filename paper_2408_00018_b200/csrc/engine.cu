@@ -1,0 +1,511 @@
+// engine.cu — the persistent synchronous engine (V2), the asynchronous
+// engine (V1/V0), and the device probes used by the parity tests.
+//
+// Synchronous engine (engines.cpp:131-207) as ONE cooperative kernel:
+//
+//   for each level l (engines.cpp:171):
+//     every thread sweeps its chains c = gtid, gtid + G*B, ... from the
+//       level start x*_l: cache V := V*, N Metropolis trials on stream
+//       (seed, c, l) with the term-cached energy, accept bits -> masks;
+//     warp-shuffle -> block argmin -> cand[l&1][block]          (:187-190)
+//     grid.sync()
+//     every block: argmin over cand[l&1][*] (identical in all blocks), then
+//       rebuilds x*_{l+1} by replaying the winner's accepted moves from its
+//       accept mask and stream (no chain state leaves the SM), recomputes
+//       V* = cache(x*_{l+1}); block 0 keeps best-so-far and the trace
+//       (:191-198).
+//
+// One grid-wide barrier per level; cand and masks are double-buffered by
+// level parity so a block that runs ahead cannot overwrite data a slower
+// block is still reading.
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include <stdint.h>
+
+#include "engine.cuh"
+#include "engine_host.h"
+
+namespace cg = cooperative_groups;
+
+namespace psa {
+
+// ---------------------------------------------------------------------------
+// shared-memory carve-up
+// ---------------------------------------------------------------------------
+
+struct Smem {
+    unsigned char* base;
+    size_t off = 0;
+    template <class T>
+    __device__ T* take(size_t count) {
+        off = (off + 15) & ~size_t(15);
+        T* p = reinterpret_cast<T*>(base + off);
+        off += sizeof(T) * count;
+        return p;
+    }
+};
+
+template <class R, int A>
+size_t engine_smem_bytes(int n, int B, bool with_x) {
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        off = (off + 15) & ~size_t(15);
+        off += bytes;
+    };
+    take(sizeof(R) * size_t(n) * A * B); // V
+    if (with_x) take(sizeof(double) * size_t(n) * B); // per-thread x (async engine)
+    take(sizeof(double) * n);            // x*
+    take(sizeof(R) * size_t(n) * A);     // V*
+    take(sizeof(double) * n);            // lower
+    take(sizeof(double) * n);            // width
+    take(sizeof(Cand) * 34);             // reduction scratch
+    take(64);                            // scalars
+    return off;
+}
+
+struct SharedScalars {
+    double estar;
+    double best_f;
+    int32_t best_c;
+    int32_t pad;
+};
+
+template <class R, class Cost>
+__device__ void load_box(const EngineArgs& a, double* lower, double* width, Box& box) {
+    for (int k = threadIdx.x; k < a.n; k += blockDim.x) {
+        if (!a.uniform_box) {
+            lower[k] = a.lower[k];
+            width[k] = a.width[k];
+        }
+    }
+    box.lower = lower;
+    box.width = width;
+    box.lo0 = a.lo0;
+    box.w0 = a.w0;
+    box.uniform = a.uniform_box != 0;
+}
+
+// cache values of point xs (shared, n doubles) into vs (shared, n*A)
+template <class R, class Cost>
+__device__ void cache_point(const double* xs, R* vs, int n, int family) {
+    constexpr int A = Cost::A;
+    for (int k = threadIdx.x; k < n; k += blockDim.x) {
+        R t[A];
+        Cost::cache(static_cast<R>(xs[k]), k, n, t);
+#pragma unroll
+        for (int q = 0; q < A; ++q) vs[k * A + q] = t[q];
+    }
+    (void)family;
+}
+
+// draw_random_start (engines.cpp:43-46): coordinate k uses draw k of (seed, c, 0)
+__device__ __forceinline__ double random_start_coord(const EngineArgs& a, const Box& box,
+                                                     uint32_t c, int k) {
+    const uint64_t m = draw_bits53(static_cast<uint64_t>(k), c, 0, a.keys);
+    return box.point(k, bits_to_uniform(m));
+}
+
+// Rebuild the end point of chain `cw` at level l into xs (shared), starting
+// from the level's start point already in xs.  Warp 0 only.
+__device__ void replay_winner(const EngineArgs& a, const Box& box, double* xs, int level,
+                              int32_t cw, const uint32_t* masks) {
+    if (threadIdx.x >= 32) return;
+    const int lane = threadIdx.x;
+    const int W = (a.N + 31) / 32;
+    const uint64_t ctr0 = (level == 0 && a.random_start) ? static_cast<uint64_t>(a.n) : 0;
+    const size_t cl = static_cast<size_t>(cw - a.chain_begin);
+    for (int w = 0; w < W; ++w) {
+        const uint32_t word = masks[static_cast<size_t>(w) * a.chains_local + cl];
+        const int j = w * 32 + lane;
+        const bool acc = j < a.N && ((word >> lane) & 1u);
+        int d = -1;
+        double xv = 0;
+        if (acc) {
+            const uint64_t base = ctr0 + 3ull * static_cast<uint64_t>(j);
+            const uint64_t m1 = draw_bits53(base, static_cast<uint32_t>(cw), level, a.keys);
+            d = coordinate_index(bits_to_uniform(m1), a.n);
+            const uint64_t m2 = draw_bits53(base + 1, static_cast<uint32_t>(cw), level, a.keys);
+            xv = box.point(d, bits_to_uniform(m2));
+        }
+        const unsigned am = __ballot_sync(0xffffffffu, acc);
+        if (acc) {
+            const unsigned same = __match_any_sync(am, d);
+            if (31 - __clz(same) == lane) xs[d] = xv; // last accepted write per coordinate
+        }
+        __syncwarp();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// V2 persistent kernel
+// ---------------------------------------------------------------------------
+
+template <class R, class Cost>
+__global__ void __launch_bounds__(256) v2_kernel(const EngineArgs a) {
+    constexpr int A = Cost::A;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    cg::grid_group grid = cg::this_grid();
+    const int B = blockDim.x, tid = threadIdx.x;
+    const int n = a.n;
+    Smem sm{smem_raw};
+    R* V = sm.take<R>(static_cast<size_t>(n) * A * B);
+    double* xs = sm.take<double>(n);
+    R* vs = sm.take<R>(static_cast<size_t>(n) * A);
+    double* lower = sm.take<double>(n);
+    double* width = sm.take<double>(n);
+    Cand* scratch = sm.take<Cand>(34);
+    SharedScalars* sh = sm.take<SharedScalars>(1);
+
+    Box box;
+    load_box<R, Cost>(a, lower, width, box);
+    for (int k = tid; k < n; k += B) xs[k] = a.start[k];
+    __syncthreads();
+    cache_point<R, Cost>(xs, vs, n, a.family);
+    __syncthreads();
+    if (tid == 0) {
+        sh->estar = static_cast<double>(Cost::energy(vs, 1, n, a.family));
+        sh->best_f = __longlong_as_double(0x7ff0000000000000ll);
+        sh->best_c = 0;
+    }
+    __syncthreads();
+
+    const size_t total_threads = static_cast<size_t>(gridDim.x) * B;
+    const size_t gtid = static_cast<size_t>(blockIdx.x) * B + tid;
+    const size_t W = static_cast<size_t>((a.N + 31) / 32);
+    const size_t mask_buf = W * a.chains_local;
+    R* col = V + tid;
+    SweepStats st{0, 0};
+
+    for (int l = 0; l < a.levels; ++l) {
+        const double temperature = a.temps[l];
+        const R estar = static_cast<R>(sh->estar);
+        uint32_t* masks = a.masks + static_cast<size_t>(l & 1) * mask_buf;
+        Cand best = empty_cand(), sbest = empty_cand();
+        for (size_t cl = gtid; cl < a.chains_local; cl += total_threads) {
+            const uint32_t c = static_cast<uint32_t>(a.chain_begin + cl);
+            R e;
+            uint64_t ctr = 0;
+            if (l == 0 && a.random_start) {
+                for (int k = 0; k < n; ++k) {
+                    R t[A];
+                    Cost::cache(static_cast<R>(random_start_coord(a, box, c, k)), k, n, t);
+#pragma unroll
+                    for (int q = 0; q < A; ++q) col[static_cast<size_t>(k * A + q) * B] = t[q];
+                }
+                e = Cost::energy(col, B, n, a.family);
+                ctr = static_cast<uint64_t>(n);
+                st.draws += static_cast<uint64_t>(n);
+                const Cand s{static_cast<double>(e), static_cast<int32_t>(c), 0};
+                if (better(s, sbest)) sbest = s;
+            } else {
+                for (int k = 0; k < n * A; ++k) col[static_cast<size_t>(k) * B] = vs[k];
+                e = estar;
+            }
+            if (l == 0) st.evals += 1; // the start evaluation (engines.cpp:157)
+            e = sweep<R, Cost>(col, B, n, a.family, e, temperature, c, static_cast<uint32_t>(l), ctr,
+                               a.N, box, a.keys, masks + cl, a.chains_local, nullptr, st);
+            const Cand mine{static_cast<double>(e), static_cast<int32_t>(c), 0};
+            if (better(mine, best)) best = mine;
+        }
+        // block argmin -> cand[l&1][block]
+        best = block_argmin(best, scratch);
+        if (l == 0 && a.random_start) sbest = block_argmin(sbest, scratch);
+        if (tid == 0) {
+            a.cand[static_cast<size_t>(l & 1) * gridDim.x + blockIdx.x] = best;
+            if (l == 0 && a.random_start) a.cand_start[blockIdx.x] = sbest;
+        }
+        grid.sync();
+
+        // every block: global argmin over the block candidates
+        Cand w = empty_cand(), ws = empty_cand();
+        for (int i = tid; i < static_cast<int>(gridDim.x); i += B) {
+            const Cand c = a.cand[static_cast<size_t>(l & 1) * gridDim.x + i];
+            if (better(c, w)) w = c;
+            if (l == 0 && a.random_start) {
+                const Cand s = a.cand_start[i];
+                if (better(s, ws)) ws = s;
+            }
+        }
+        w = block_argmin(w, scratch);
+        if (l == 0 && a.random_start) ws = block_argmin(ws, scratch);
+
+        // level-0 best-so-far: the start scan (engines.cpp:161-167)
+        if (l == 0 && blockIdx.x == 0) {
+            if (a.random_start) {
+                for (int k = tid; k < n; k += B) a.best_x[k] = random_start_coord(a, box, ws.c, k);
+                if (tid == 0) { sh->best_f = ws.e; sh->best_c = ws.c; }
+            } else {
+                for (int k = tid; k < n; k += B) a.best_x[k] = xs[k];
+                if (tid == 0) { sh->best_f = sh->estar; sh->best_c = 0; }
+            }
+        }
+        // the level's start point of the winner -> xs
+        if (l == 0 && a.random_start)
+            for (int k = tid; k < n; k += B) xs[k] = random_start_coord(a, box, w.c, k);
+        __syncthreads();
+        replay_winner(a, box, xs, l, w.c, masks);
+        __syncthreads();
+        cache_point<R, Cost>(xs, vs, n, a.family);
+        if (tid == 0) sh->estar = w.e;
+        __syncthreads();
+        if (blockIdx.x == 0) {
+            const bool improve = w.e < sh->best_f; // engines.cpp:193 (strict)
+            if (improve)
+                for (int k = tid; k < n; k += B) a.best_x[k] = xs[k];
+            __syncthreads();
+            if (tid == 0) {
+                if (improve) {
+                    sh->best_f = w.e;
+                    sh->best_c = w.c;
+                }
+                a.trace_best[l] = sh->best_f;
+                if (a.level_winner) a.level_winner[l] = w.c;
+                if (a.level_winner_f) a.level_winner_f[l] = w.e;
+            }
+            __syncthreads();
+        }
+    }
+    if (blockIdx.x == 0 && tid == 0) {
+        a.out_scalars->best_f = sh->best_f;
+        a.out_scalars->best_chain = sh->best_c;
+    }
+    // accounting: device-side totals of evaluations and draws
+    __shared__ unsigned long long red_e, red_d;
+    if (tid == 0) { red_e = 0; red_d = 0; }
+    __syncthreads();
+    atomicAdd(&red_e, static_cast<unsigned long long>(st.evals));
+    atomicAdd(&red_d, static_cast<unsigned long long>(st.draws));
+    __syncthreads();
+    if (tid == 0) {
+        atomicAdd(&a.out_scalars->evaluations, red_e);
+        atomicAdd(&a.out_scalars->rng_draws, red_d);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// V1 asynchronous kernel (engines.cpp:66-123)
+// Each thread runs whole chains through the full ladder on stream (seed,c,0).
+// Per level, the block folds its chains' running best into
+// trace_cand[l][block]; at the end each thread's best end state goes to
+// cand[gtid] with its point in xbest[gtid].  v1_finalize reduces both.
+// ---------------------------------------------------------------------------
+
+template <class R, class Cost>
+__global__ void __launch_bounds__(256) v1_kernel(const EngineArgs a) {
+    constexpr int A = Cost::A;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int B = blockDim.x, tid = threadIdx.x;
+    const int n = a.n;
+    Smem sm{smem_raw};
+    R* V = sm.take<R>(static_cast<size_t>(n) * A * B);
+    double* X = sm.take<double>(static_cast<size_t>(n) * B);
+    double* xs = sm.take<double>(n);
+    R* vs = sm.take<R>(static_cast<size_t>(n) * A);
+    double* lower = sm.take<double>(n);
+    double* width = sm.take<double>(n);
+    Cand* scratch = sm.take<Cand>(34);
+    SharedScalars* sh = sm.take<SharedScalars>(1);
+
+    Box box;
+    load_box<R, Cost>(a, lower, width, box);
+    for (int k = tid; k < n; k += B) xs[k] = a.start[k];
+    __syncthreads();
+    cache_point<R, Cost>(xs, vs, n, a.family);
+    __syncthreads();
+    if (tid == 0) sh->estar = static_cast<double>(Cost::energy(vs, 1, n, a.family));
+    __syncthreads();
+
+    const size_t total_threads = static_cast<size_t>(gridDim.x) * B;
+    const size_t gtid = static_cast<size_t>(blockIdx.x) * B + tid;
+    const size_t rounds = (a.chains_local + total_threads - 1) / total_threads;
+    R* col = V + tid;
+    double* xcol = X + tid;
+    SweepStats st{0, 0};
+    Cand mybest = empty_cand();
+
+    for (size_t r = 0; r < rounds; ++r) {
+        const size_t cl = gtid + r * total_threads;
+        const bool active = cl < a.chains_local;
+        const uint32_t c = static_cast<uint32_t>(a.chain_begin + cl);
+        R e = 0;
+        uint64_t ctr = 0;
+        if (active) {
+            if (a.random_start) {
+                for (int k = 0; k < n; ++k) {
+                    const double xk = random_start_coord(a, box, c, k);
+                    xcol[static_cast<size_t>(k) * B] = xk;
+                    R t[A];
+                    Cost::cache(static_cast<R>(xk), k, n, t);
+#pragma unroll
+                    for (int q = 0; q < A; ++q) col[static_cast<size_t>(k * A + q) * B] = t[q];
+                }
+                e = Cost::energy(col, B, n, a.family);
+                ctr = static_cast<uint64_t>(n);
+                st.draws += static_cast<uint64_t>(n);
+            } else {
+                for (int k = 0; k < n; ++k) xcol[static_cast<size_t>(k) * B] = xs[k];
+                for (int k = 0; k < n * A; ++k) col[static_cast<size_t>(k) * B] = vs[k];
+                e = static_cast<R>(sh->estar);
+            }
+            st.evals += 1;
+        }
+        double chain_best = static_cast<double>(e);
+        for (int l = 0; l < a.levels; ++l) {
+            if (active) {
+                e = sweep<R, Cost>(col, B, n, a.family, e, a.temps[l], c, 0, ctr, a.N, box, a.keys,
+                                   nullptr, 0, xcol, st);
+                ctr += 3ull * static_cast<uint64_t>(a.N);
+                // std::min(chain_best, energy) (engines.cpp:94)
+                if (static_cast<double>(e) < chain_best) chain_best = static_cast<double>(e);
+            }
+            // trace: min over chains of chain_best; std::min(m, v) skips NaN and
+            // keeps the first (smallest chain) among equal values
+            Cand tv = active && !is_nan(chain_best)
+                          ? Cand{chain_best, static_cast<int32_t>(c), 0}
+                          : empty_cand();
+            tv = block_argmin(tv, scratch);
+            if (tid == 0) {
+                Cand* slot = &a.trace_cand[static_cast<size_t>(l) * gridDim.x + blockIdx.x];
+                if (r == 0 || better(tv, *slot)) *slot = tv;
+            }
+        }
+        if (active) {
+            const Cand mine{static_cast<double>(e), static_cast<int32_t>(c), static_cast<int32_t>(gtid)};
+            if (better(mine, mybest)) {
+                mybest = mine;
+                for (int k = 0; k < n; ++k)
+                    a.xbest[gtid * static_cast<size_t>(n) + k] = xcol[static_cast<size_t>(k) * B];
+            }
+        }
+    }
+    const Cand b = block_argmin(mybest, scratch);
+    if (tid == 0) a.cand[blockIdx.x] = b;
+
+    __shared__ unsigned long long red_e, red_d;
+    if (tid == 0) { red_e = 0; red_d = 0; }
+    __syncthreads();
+    atomicAdd(&red_e, static_cast<unsigned long long>(st.evals));
+    atomicAdd(&red_d, static_cast<unsigned long long>(st.draws));
+    __syncthreads();
+    if (tid == 0) {
+        atomicAdd(&a.out_scalars->evaluations, red_e);
+        atomicAdd(&a.out_scalars->rng_draws, red_d);
+    }
+}
+
+__global__ void v1_finalize(const EngineArgs a, int blocks) {
+    __shared__ Cand scratch[34];
+    const int tid = threadIdx.x;
+    Cand w = empty_cand();
+    for (int i = tid; i < blocks; i += blockDim.x)
+        if (better(a.cand[i], w)) w = a.cand[i];
+    w = block_argmin(w, scratch);
+    for (int k = tid; k < a.n; k += blockDim.x)
+        a.best_x[k] = a.xbest[static_cast<size_t>(w.aux) * a.n + k];
+    if (tid == 0) {
+        a.out_scalars->best_f = w.e;
+        a.out_scalars->best_chain = w.c;
+    }
+    for (int l = 0; l < a.levels; ++l) {
+        Cand t = empty_cand();
+        for (int i = tid; i < blocks; i += blockDim.x) {
+            const Cand c = a.trace_cand[static_cast<size_t>(l) * blocks + i];
+            if (better(c, t)) t = c;
+        }
+        t = block_argmin(t, scratch);
+        if (tid == 0) a.trace_best[l] = t.c == INT32_MAX ? __longlong_as_double(0x7ff0000000000000ll) : t.e;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Probes
+// ---------------------------------------------------------------------------
+
+__global__ void probe_uniforms(uint64_t seed, uint32_t chain, uint32_t level, uint64_t first,
+                               int count, double* out) {
+    const PhiloxKeys keys = make_keys(seed);
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < count; i += gridDim.x * blockDim.x)
+        out[i] = bits_to_uniform(draw_bits53(first + i, chain, level, keys));
+}
+
+__global__ void probe_philox(const uint32_t* ctr, uint32_t k0, uint32_t k1, int count,
+                             uint32_t* out) {
+    PhiloxKeys keys;
+    uint32_t a = k0, b = k1;
+    for (int r = 0; r < 10; ++r) {
+        keys.k0[r] = a;
+        keys.k1[r] = b;
+        a += kPhiloxW0;
+        b += kPhiloxW1;
+    }
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < count; i += gridDim.x * blockDim.x) {
+        uint32_t v[4] = {ctr[4 * i], ctr[4 * i + 1], ctr[4 * i + 2], ctr[4 * i + 3]};
+        philox4x32_10(v, keys);
+        for (int q = 0; q < 4; ++q) out[4 * i + q] = v[q];
+    }
+}
+
+// f(x_i) through the engine's own cache/energy path (one point per thread)
+template <class R, class Cost>
+__global__ void probe_evaluate(const EngineArgs a, const double* x, int count, double* out) {
+    constexpr int A = Cost::A;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    R* V = reinterpret_cast<R*>(smem_raw);
+    const int B = blockDim.x;
+    R* col = V + threadIdx.x;
+    const int i = blockIdx.x * B + threadIdx.x;
+    if (i >= count) return;
+    for (int k = 0; k < a.n; ++k) {
+        R t[A];
+        Cost::cache(static_cast<R>(x[static_cast<size_t>(i) * a.n + k]), k, a.n, t);
+#pragma unroll
+        for (int q = 0; q < A; ++q) col[static_cast<size_t>(k * A + q) * B] = t[q];
+    }
+    out[i] = static_cast<double>(Cost::energy(col, B, a.n, a.family));
+}
+
+// ---------------------------------------------------------------------------
+// Host-side dispatch over (precision, family)
+// ---------------------------------------------------------------------------
+
+template <class R, class Cost>
+struct KernelSet {
+    static EngineKernels get() {
+        EngineKernels k;
+        k.v2 = reinterpret_cast<const void*>(&v2_kernel<R, Cost>);
+        k.v1 = reinterpret_cast<const void*>(&v1_kernel<R, Cost>);
+        k.eval = reinterpret_cast<const void*>(&probe_evaluate<R, Cost>);
+        k.smem_v2 = [](int n, int B) { return engine_smem_bytes<R, Cost::A>(n, B, false); };
+        k.smem_v1 = [](int n, int B) { return engine_smem_bytes<R, Cost::A>(n, B, true); };
+        k.smem_eval = [](int n, int B) { return sizeof(R) * size_t(n) * Cost::A * B; };
+        return k;
+    }
+};
+
+template <class R>
+EngineKernels kernels_for(int family) {
+    switch (family) {
+    case PSA_FN_SCHWEFEL: return KernelSet<R, SepCost<R, Schwefel>>::get();
+    case PSA_FN_ACKLEY: return KernelSet<R, SepCost<R, Ackley>>::get();
+    case PSA_FN_COSINE_MIXTURE: return KernelSet<R, SepCost<R, CosineMixture>>::get();
+    case PSA_FN_EXPONENTIAL: return KernelSet<R, SepCost<R, Exponential>>::get();
+    case PSA_FN_GRIEWANK: return KernelSet<R, SepCost<R, Griewank>>::get();
+    case PSA_FN_MICHALEWICZ: return KernelSet<R, SepCost<R, Michalewicz>>::get();
+    case PSA_FN_RASTRIGIN: return KernelSet<R, SepCost<R, Rastrigin>>::get();
+    case PSA_FN_SALOMON: return KernelSet<R, SepCost<R, Salomon>>::get();
+    case PSA_FN_SHUBERT: return KernelSet<R, SepCost<R, Shubert>>::get();
+    case PSA_FN_SPHERE: return KernelSet<R, SepCost<R, Sphere>>::get();
+    default: return KernelSet<R, FullCost<R>>::get();
+    }
+}
+
+EngineKernels engine_kernels(int precision, int family) {
+    return precision == PSA_F32 ? kernels_for<float>(family) : kernels_for<double>(family);
+}
+
+const void* probe_uniforms_kernel() { return reinterpret_cast<const void*>(&probe_uniforms); }
+const void* probe_philox_kernel() { return reinterpret_cast<const void*>(&probe_philox); }
+const void* v1_finalize_kernel() { return reinterpret_cast<const void*>(&v1_finalize); }
+
+} // namespace psa

@@ -1,0 +1,71 @@
+// engine_host.h — plain structs shared by the kernels (engine.cu) and the
+// host driver (capi.cu).
+#pragma once
+
+#include <stddef.h>
+#include <stdint.h>
+
+#include "parsa_b200.h"
+#include "philox.cuh"
+
+namespace psa {
+
+// candidate for the argmin reductions (see engine.cuh: better())
+struct Cand {
+    double e;
+    int32_t c;   // global chain index, INT32_MAX = empty
+    int32_t aux; // asynchronous engine: owning thread
+};
+
+struct OutScalars {
+    double best_f;
+    int32_t best_chain;
+    int32_t pad;
+    unsigned long long evaluations;
+    unsigned long long rng_draws;
+};
+
+// Kernel arguments (passed by value; all pointers are device pointers).
+struct EngineArgs {
+    int n;
+    int family;
+    int N;      // sweep_length
+    int levels;
+    int uniform_box;
+    int random_start;
+    double lo0, w0;
+    const double* lower;
+    const double* width;
+    const double* start;
+    const double* temps;
+    PhiloxKeys keys;
+    size_t chains_local;   // chains in this shard
+    uint32_t chain_begin;  // global index of the shard's first chain
+    uint32_t chains_total;
+    uint32_t* masks;       // V2: [2][ceil(N/32)][chains_local] accept bits
+    Cand* cand;            // V2: [2][grid]; V1: [grid]
+    Cand* cand_start;      // V2 random start: [grid]
+    Cand* trace_cand;      // V1: [levels][grid]
+    double* trace_best;    // [levels]
+    double* best_x;        // [n]
+    double* xbest;         // V1: [grid*B][n]
+    int32_t* level_winner; // V2: [levels] (diagnostic)
+    double* level_winner_f;
+    OutScalars* out_scalars;
+};
+
+struct EngineKernels {
+    const void* v2;
+    const void* v1;
+    const void* eval;
+    size_t (*smem_v2)(int n, int B);
+    size_t (*smem_v1)(int n, int B);
+    size_t (*smem_eval)(int n, int B);
+};
+
+EngineKernels engine_kernels(int precision, int family);
+const void* probe_uniforms_kernel();
+const void* probe_philox_kernel();
+const void* v1_finalize_kernel();
+
+} // namespace psa

@@ -1,0 +1,90 @@
+// philox.cuh — counter-based streams, bit-identical to the reference.
+//
+// Reference: rng.hpp:13-18 (bit spec), :30-33 (constants), :39-52 (cipher),
+// :66-81 (uniform and coordinate index).  Draw i of stream (seed, chain,
+// level) is philox4x32_10({lo32(i), hi32(i), chain, level}, {lo32(seed),
+// hi32(seed)}); only out[0], out[1] are used.
+//
+// Device layout: the ten round keys depend on the seed only, so the host
+// precomputes them once (PhiloxKeys) and they reach the kernel as uniform
+// kernel parameters; a draw then costs 10 x (2 IMAD.WIDE.U32 + 2 LOP3), with
+// the dead half of the last round eliminated.
+#pragma once
+
+#include <stdint.h>
+
+#ifndef PSA_HD
+#define PSA_HD __host__ __device__ __forceinline__
+#endif
+
+namespace psa {
+
+constexpr uint32_t kPhiloxM0 = 0xD2511F53u;
+constexpr uint32_t kPhiloxM1 = 0xCD9E8D57u;
+constexpr uint32_t kPhiloxW0 = 0x9E3779B9u;
+constexpr uint32_t kPhiloxW1 = 0xBB67AE85u;
+
+struct PhiloxKeys {
+    uint32_t k0[10];
+    uint32_t k1[10];
+};
+
+PSA_HD PhiloxKeys make_keys(uint64_t seed) {
+    PhiloxKeys k;
+    uint32_t a = static_cast<uint32_t>(seed), b = static_cast<uint32_t>(seed >> 32);
+    for (int r = 0; r < 10; ++r) {
+        k.k0[r] = a;
+        k.k1[r] = b;
+        a += kPhiloxW0;
+        b += kPhiloxW1;
+    }
+    return k;
+}
+
+PSA_HD void mulhilo(uint32_t a, uint32_t m, uint32_t& hi, uint32_t& lo) {
+    const uint64_t p = static_cast<uint64_t>(m) * a;
+    hi = static_cast<uint32_t>(p >> 32);
+    lo = static_cast<uint32_t>(p);
+}
+
+// Full 4x32 block (used by the KAT probe).
+PSA_HD void philox4x32_10(uint32_t v[4], const PhiloxKeys& key) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        uint32_t hi0, lo0, hi1, lo1;
+        mulhilo(v[0], kPhiloxM0, hi0, lo0);
+        mulhilo(v[2], kPhiloxM1, hi1, lo1);
+        const uint32_t n0 = hi1 ^ v[1] ^ key.k0[r];
+        const uint32_t n2 = hi0 ^ v[3] ^ key.k1[r];
+        v[0] = n0;
+        v[1] = lo1;
+        v[2] = n2;
+        v[3] = lo0;
+    }
+}
+
+// The 53-bit mantissa integer m of draw `counter`: u = m * 2^-53
+// (rng.hpp:72-74: bits = out1<<32 | out0; u = (bits >> 11) * 2^-53).
+PSA_HD uint64_t draw_bits53(uint64_t counter, uint32_t chain, uint32_t level,
+                            const PhiloxKeys& key) {
+    uint32_t v[4] = {static_cast<uint32_t>(counter), static_cast<uint32_t>(counter >> 32), chain,
+                     level};
+    philox4x32_10(v, key);
+    const uint64_t bits = (static_cast<uint64_t>(v[1]) << 32) | static_cast<uint64_t>(v[0]);
+    return bits >> 11;
+}
+
+PSA_HD double bits_to_uniform(uint64_t m) { return static_cast<double>(m) * 0x1.0p-53; }
+
+// rng.hpp:78-81 — d = int(u * n), clamped to n-1; u*n is one IEEE multiply.
+PSA_HD int coordinate_index(double u, int n) {
+    const int d = static_cast<int>(u * static_cast<double>(n));
+    return d < n ? d : n - 1;
+}
+
+// float(u) for the single-precision Metropolis test (sa_core.cpp:51-53):
+// rounding m to 24 bits then scaling by 2^-53 is exact, so this equals
+// static_cast<float>(m * 2^-53) without a double round trip.
+PSA_HD float bits_to_uniform_f32(uint64_t m) { return static_cast<float>(m) * 0x1.0p-53f; }
+
+} // namespace psa
