@@ -215,7 +215,7 @@ void plan_build(psa_plan* p, const psa_objective* f, const psa_engine_config* cf
     p->chains_local = chain_end - chain_begin;
     p->chains_total = static_cast<uint32_t>(cfg->n_chains);
     p->random_start = cfg->start_mode == PSA_RANDOM_PER_CHAIN;
-    p->ks = psa::engine_kernels(p->precision, p->family);
+    p->ks = psa::engine_kernels(p->precision, p->family, f->dim);
 
     const int n = p->n;
     std::vector<double> width(n);
@@ -299,6 +299,11 @@ void plan_build(psa_plan* p, const psa_objective* f, const psa_engine_config* cf
     a.level_winner = p->d_winner.p;
     a.level_winner_f = p->d_winner_f.p;
     a.out_scalars = p->d_out.p;
+
+    // the device keeps per-stream draw counters in 32 bits (philox.cuh)
+    const uint64_t max_draw = static_cast<uint64_t>(n) + 3ull * p->N * (engine == 1 ? p->levels : 1) + 8;
+    if (max_draw >= (1ull << 32))
+        fail(PSA_ERR_INVALID_ARGUMENT, "parsa_b200: more than 2^32 draws per stream is not supported");
 
     // engines.cpp:48-51 / sa_core.cpp:29-35
     p->expected_evals = static_cast<uint64_t>(p->chains_local) *
@@ -518,7 +523,7 @@ psa_status psa_device_evaluate(const psa_objective* f, int32_t precision, const 
         check_objective(f);
         require_device();
         const int n = f->dim;
-        const EngineKernels ks = psa::engine_kernels(precision == PSA_F32 ? PSA_F32 : PSA_F64, f->family);
+        const EngineKernels ks = psa::engine_kernels(precision == PSA_F32 ? PSA_F32 : PSA_F64, f->family, 0);
         int B = 64;
         while (B > 1 && ks.smem_eval(n, B) > 160 * 1024) B /= 2;
         const size_t smem = ks.smem_eval(n, B);

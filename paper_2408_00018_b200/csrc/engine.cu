@@ -53,8 +53,8 @@ size_t engine_smem_bytes(int n, int B, bool with_x) {
         off = (off + 15) & ~size_t(15);
         off += bytes;
     };
-    take(sizeof(R) * size_t(n) * A * B); // V
-    if (with_x) take(sizeof(double) * size_t(n) * B); // per-thread x (async engine)
+    take(sizeof(R) * size_t(row_stride<R>(n, A)) * B); // per-thread state rows
+    if (with_x) take(sizeof(double) * size_t(n) * B);    // per-thread x (async engine)
     take(sizeof(double) * n);            // x*
     take(sizeof(R) * size_t(n) * A);     // V*
     take(sizeof(double) * n);            // lower
@@ -141,7 +141,7 @@ __device__ void replay_winner(const EngineArgs& a, const Box& box, double* xs, i
 // V2 persistent kernel
 // ---------------------------------------------------------------------------
 
-template <class R, class Cost>
+template <class R, class Cost, int NT>
 __global__ void __launch_bounds__(256) v2_kernel(const EngineArgs a) {
     constexpr int A = Cost::A;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -149,7 +149,8 @@ __global__ void __launch_bounds__(256) v2_kernel(const EngineArgs a) {
     const int B = blockDim.x, tid = threadIdx.x;
     const int n = a.n;
     Smem sm{smem_raw};
-    R* V = sm.take<R>(static_cast<size_t>(n) * A * B);
+    const int S = row_stride<R>(n, A);
+    R* V = sm.take<R>(static_cast<size_t>(S) * B);
     double* xs = sm.take<double>(n);
     R* vs = sm.take<R>(static_cast<size_t>(n) * A);
     double* lower = sm.take<double>(n);
@@ -164,7 +165,7 @@ __global__ void __launch_bounds__(256) v2_kernel(const EngineArgs a) {
     cache_point<R, Cost>(xs, vs, n, a.family);
     __syncthreads();
     if (tid == 0) {
-        sh->estar = static_cast<double>(Cost::energy(vs, 1, n, a.family));
+        sh->estar = static_cast<double>(Cost::template energy<NT>(vs, n, a.family));
         sh->best_f = __longlong_as_double(0x7ff0000000000000ll);
         sh->best_c = 0;
     }
@@ -174,7 +175,7 @@ __global__ void __launch_bounds__(256) v2_kernel(const EngineArgs a) {
     const size_t gtid = static_cast<size_t>(blockIdx.x) * B + tid;
     const size_t W = static_cast<size_t>((a.N + 31) / 32);
     const size_t mask_buf = W * a.chains_local;
-    R* col = V + tid;
+    R* row = V + static_cast<size_t>(tid) * S;
     SweepStats st{0, 0};
 
     for (int l = 0; l < a.levels; ++l) {
@@ -185,25 +186,25 @@ __global__ void __launch_bounds__(256) v2_kernel(const EngineArgs a) {
         for (size_t cl = gtid; cl < a.chains_local; cl += total_threads) {
             const uint32_t c = static_cast<uint32_t>(a.chain_begin + cl);
             R e;
-            uint64_t ctr = 0;
+            uint32_t ctr = 0;
             if (l == 0 && a.random_start) {
                 for (int k = 0; k < n; ++k) {
                     R t[A];
                     Cost::cache(static_cast<R>(random_start_coord(a, box, c, k)), k, n, t);
 #pragma unroll
-                    for (int q = 0; q < A; ++q) col[static_cast<size_t>(k * A + q) * B] = t[q];
+                    for (int q = 0; q < A; ++q) row[k * A + q] = t[q];
                 }
-                e = Cost::energy(col, B, n, a.family);
-                ctr = static_cast<uint64_t>(n);
+                e = Cost::template energy<NT>(row, n, a.family);
+                ctr = static_cast<uint32_t>(n);
                 st.draws += static_cast<uint64_t>(n);
                 const Cand s{static_cast<double>(e), static_cast<int32_t>(c), 0};
                 if (better(s, sbest)) sbest = s;
             } else {
-                for (int k = 0; k < n * A; ++k) col[static_cast<size_t>(k) * B] = vs[k];
+                for (int k = 0; k < n * A; ++k) row[k] = vs[k];
                 e = estar;
             }
             if (l == 0) st.evals += 1; // the start evaluation (engines.cpp:157)
-            e = sweep<R, Cost>(col, B, n, a.family, e, temperature, c, static_cast<uint32_t>(l), ctr,
+            e = sweep<R, Cost, NT>(row, n, a.family, e, temperature, c, static_cast<uint32_t>(l), ctr,
                                a.N, box, a.keys, masks + cl, a.chains_local, nullptr, st);
             const Cand mine{static_cast<double>(e), static_cast<int32_t>(c), 0};
             if (better(mine, best)) best = mine;
@@ -291,14 +292,15 @@ __global__ void __launch_bounds__(256) v2_kernel(const EngineArgs a) {
 // cand[gtid] with its point in xbest[gtid].  v1_finalize reduces both.
 // ---------------------------------------------------------------------------
 
-template <class R, class Cost>
+template <class R, class Cost, int NT>
 __global__ void __launch_bounds__(256) v1_kernel(const EngineArgs a) {
     constexpr int A = Cost::A;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int B = blockDim.x, tid = threadIdx.x;
     const int n = a.n;
     Smem sm{smem_raw};
-    R* V = sm.take<R>(static_cast<size_t>(n) * A * B);
+    const int S = row_stride<R>(n, A);
+    R* V = sm.take<R>(static_cast<size_t>(S) * B);
     double* X = sm.take<double>(static_cast<size_t>(n) * B);
     double* xs = sm.take<double>(n);
     R* vs = sm.take<R>(static_cast<size_t>(n) * A);
@@ -313,14 +315,14 @@ __global__ void __launch_bounds__(256) v1_kernel(const EngineArgs a) {
     __syncthreads();
     cache_point<R, Cost>(xs, vs, n, a.family);
     __syncthreads();
-    if (tid == 0) sh->estar = static_cast<double>(Cost::energy(vs, 1, n, a.family));
+    if (tid == 0) sh->estar = static_cast<double>(Cost::template energy<NT>(vs, n, a.family));
     __syncthreads();
 
     const size_t total_threads = static_cast<size_t>(gridDim.x) * B;
     const size_t gtid = static_cast<size_t>(blockIdx.x) * B + tid;
     const size_t rounds = (a.chains_local + total_threads - 1) / total_threads;
-    R* col = V + tid;
-    double* xcol = X + tid;
+    R* row = V + static_cast<size_t>(tid) * S;
+    double* xrow = X + static_cast<size_t>(tid) * n;
     SweepStats st{0, 0};
     Cand mybest = empty_cand();
 
@@ -329,23 +331,23 @@ __global__ void __launch_bounds__(256) v1_kernel(const EngineArgs a) {
         const bool active = cl < a.chains_local;
         const uint32_t c = static_cast<uint32_t>(a.chain_begin + cl);
         R e = 0;
-        uint64_t ctr = 0;
+        uint32_t ctr = 0;
         if (active) {
             if (a.random_start) {
                 for (int k = 0; k < n; ++k) {
                     const double xk = random_start_coord(a, box, c, k);
-                    xcol[static_cast<size_t>(k) * B] = xk;
+                    xrow[k] = xk;
                     R t[A];
                     Cost::cache(static_cast<R>(xk), k, n, t);
 #pragma unroll
-                    for (int q = 0; q < A; ++q) col[static_cast<size_t>(k * A + q) * B] = t[q];
+                    for (int q = 0; q < A; ++q) row[k * A + q] = t[q];
                 }
-                e = Cost::energy(col, B, n, a.family);
-                ctr = static_cast<uint64_t>(n);
+                e = Cost::template energy<NT>(row, n, a.family);
+                ctr = static_cast<uint32_t>(n);
                 st.draws += static_cast<uint64_t>(n);
             } else {
-                for (int k = 0; k < n; ++k) xcol[static_cast<size_t>(k) * B] = xs[k];
-                for (int k = 0; k < n * A; ++k) col[static_cast<size_t>(k) * B] = vs[k];
+                for (int k = 0; k < n; ++k) xrow[k] = xs[k];
+                for (int k = 0; k < n * A; ++k) row[k] = vs[k];
                 e = static_cast<R>(sh->estar);
             }
             st.evals += 1;
@@ -353,9 +355,9 @@ __global__ void __launch_bounds__(256) v1_kernel(const EngineArgs a) {
         double chain_best = static_cast<double>(e);
         for (int l = 0; l < a.levels; ++l) {
             if (active) {
-                e = sweep<R, Cost>(col, B, n, a.family, e, a.temps[l], c, 0, ctr, a.N, box, a.keys,
-                                   nullptr, 0, xcol, st);
-                ctr += 3ull * static_cast<uint64_t>(a.N);
+                e = sweep<R, Cost, NT>(row, n, a.family, e, a.temps[l], c, 0, ctr, a.N, box, a.keys,
+                                   nullptr, 0, xrow, st);
+                ctr += 3u * static_cast<uint32_t>(a.N);
                 // std::min(chain_best, energy) (engines.cpp:94)
                 if (static_cast<double>(e) < chain_best) chain_best = static_cast<double>(e);
             }
@@ -375,7 +377,7 @@ __global__ void __launch_bounds__(256) v1_kernel(const EngineArgs a) {
             if (better(mine, mybest)) {
                 mybest = mine;
                 for (int k = 0; k < n; ++k)
-                    a.xbest[gtid * static_cast<size_t>(n) + k] = xcol[static_cast<size_t>(k) * B];
+                    a.xbest[gtid * static_cast<size_t>(n) + k] = xrow[k];
             }
         }
     }
@@ -453,40 +455,52 @@ __global__ void probe_evaluate(const EngineArgs a, const double* x, int count, d
     extern __shared__ __align__(16) unsigned char smem_raw[];
     R* V = reinterpret_cast<R*>(smem_raw);
     const int B = blockDim.x;
-    R* col = V + threadIdx.x;
+    R* row = V + static_cast<size_t>(threadIdx.x) * row_stride<R>(a.n, A);
     const int i = blockIdx.x * B + threadIdx.x;
     if (i >= count) return;
     for (int k = 0; k < a.n; ++k) {
         R t[A];
         Cost::cache(static_cast<R>(x[static_cast<size_t>(i) * a.n + k]), k, a.n, t);
 #pragma unroll
-        for (int q = 0; q < A; ++q) col[static_cast<size_t>(k * A + q) * B] = t[q];
+        for (int q = 0; q < A; ++q) row[k * A + q] = t[q];
     }
-    out[i] = static_cast<double>(Cost::energy(col, B, a.n, a.family));
+    out[i] = static_cast<double>(Cost::template energy<0>(row, a.n, a.family));
 }
 
 // ---------------------------------------------------------------------------
 // Host-side dispatch over (precision, family)
 // ---------------------------------------------------------------------------
 
-template <class R, class Cost>
+template <class R, class Cost, int NT = 0>
 struct KernelSet {
     static EngineKernels get() {
         EngineKernels k;
-        k.v2 = reinterpret_cast<const void*>(&v2_kernel<R, Cost>);
-        k.v1 = reinterpret_cast<const void*>(&v1_kernel<R, Cost>);
+        k.v2 = reinterpret_cast<const void*>(&v2_kernel<R, Cost, NT>);
+        k.v1 = reinterpret_cast<const void*>(&v1_kernel<R, Cost, NT>);
         k.eval = reinterpret_cast<const void*>(&probe_evaluate<R, Cost>);
         k.smem_v2 = [](int n, int B) { return engine_smem_bytes<R, Cost::A>(n, B, false); };
         k.smem_v1 = [](int n, int B) { return engine_smem_bytes<R, Cost::A>(n, B, true); };
-        k.smem_eval = [](int n, int B) { return sizeof(R) * size_t(n) * Cost::A * B; };
+        k.smem_eval = [](int n, int B) { return sizeof(R) * size_t(row_stride<R>(n, Cost::A)) * B; };
         return k;
     }
 };
 
+// Dimensions of the benchmark configurations get a compile-time n
+// (BASELINE.json: n = 10, 30, 100).
+template <class R, template <class> class F>
+EngineKernels sep_kernels(int n) {
+    switch (n) {
+    case 10: return KernelSet<R, SepCost<R, F>, 10>::get();
+    case 30: return KernelSet<R, SepCost<R, F>, 30>::get();
+    case 100: return KernelSet<R, SepCost<R, F>, 100>::get();
+    default: return KernelSet<R, SepCost<R, F>>::get();
+    }
+}
+
 template <class R>
-EngineKernels kernels_for(int family) {
+EngineKernels kernels_for(int family, int n) {
     switch (family) {
-    case PSA_FN_SCHWEFEL: return KernelSet<R, SepCost<R, Schwefel>>::get();
+    case PSA_FN_SCHWEFEL: return sep_kernels<R, Schwefel>(n);
     case PSA_FN_ACKLEY: return KernelSet<R, SepCost<R, Ackley>>::get();
     case PSA_FN_COSINE_MIXTURE: return KernelSet<R, SepCost<R, CosineMixture>>::get();
     case PSA_FN_EXPONENTIAL: return KernelSet<R, SepCost<R, Exponential>>::get();
@@ -500,8 +514,8 @@ EngineKernels kernels_for(int family) {
     }
 }
 
-EngineKernels engine_kernels(int precision, int family) {
-    return precision == PSA_F32 ? kernels_for<float>(family) : kernels_for<double>(family);
+EngineKernels engine_kernels(int precision, int family, int n) {
+    return precision == PSA_F32 ? kernels_for<float>(family, n) : kernels_for<double>(family, n);
 }
 
 const void* probe_uniforms_kernel() { return reinterpret_cast<const void*>(&probe_uniforms); }

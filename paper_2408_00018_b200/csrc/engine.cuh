@@ -5,12 +5,7 @@
 //   * sweep()        : sa_core.cpp:61-79, one chain, N trials, term-cached
 //   * better()/argmin: engines.cpp:55-64 / :187-190 selection semantics
 //
-// Chain state layout (shared memory, structure-of-arrays): the cached value a
-// of coordinate k for the thread `t` of a block of B threads lives at
-// V[(k*A + a)*B + t], so the fold over k reads one 4- or 8-byte word per lane
-// per step, consecutive lanes hit consecutive banks (conflict-free), and a
-// proposal's scattered write V[(d*A+a)*B + t] is conflict-free too because the
-// bank depends only on t.
+// Chain state layout: see "Chain-state rows" below.
 #pragma once
 
 #include <stdint.h>
@@ -22,6 +17,40 @@
 namespace psa {
 
 // ---------------------------------------------------------------------------
+// Chain-state rows
+//
+// Each thread owns one contiguous row of S cached values (R elements) in
+// shared memory: value a of coordinate k at row[k*A + a].  S is padded so the
+// row stride is 4 (mod 8) 32-bit words: a warp's 16-byte loads of the same
+// offset then fall into distinct bank quads (conflict-free LDS.128), and the
+// fold addresses every element with an immediate offset from one base
+// register.  16 bytes carry 4 f32 or 2 f64 terms.
+// ---------------------------------------------------------------------------
+
+template <class R>
+PSA_HD int row_stride(int n, int A) {
+    int words = n * A * static_cast<int>(sizeof(R) / 4);
+    words = (words + 3) & ~3;         // whole 16-byte vectors
+    if ((words & 7) == 0) words += 4; // stride = 4 (mod 8) words
+    return words / static_cast<int>(sizeof(R) / 4);
+}
+
+template <class R>
+struct Vec16;
+template <>
+struct Vec16<float> {
+    using T = float4;
+    static constexpr int W = 4;
+    PSA_DEV static float get(const float4& v, int i) { return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w; }
+};
+template <>
+struct Vec16<double> {
+    using T = double2;
+    static constexpr int W = 2;
+    PSA_DEV static double get(const double2& v, int i) { return i == 0 ? v.x : v.y; }
+};
+
+// ---------------------------------------------------------------------------
 // Cost interface
 // ---------------------------------------------------------------------------
 
@@ -29,36 +58,58 @@ template <class R, template <class> class F>
 struct SepCost {
     using Fam = F<R>;
     static constexpr int A = Fam::kArrays;
+    static_assert(Vec16<R>::W % A == 0, "array count must divide the vector width");
     PSA_DEV static void cache(R x, int k, int, R* t) { Fam::term(x, k, t); }
-    // fold over the column V (stride B), reference order k = 0..n-1
-    PSA_DEV static R energy(const R* V, int B, int n, int) {
+    // fold over a 16-byte aligned row, reference order k = 0..n-1 per array.
+    // NT > 0: the dimension is a compile-time constant and the fold is one
+    // straight-line block (no loop), so the scheduler can interleave the
+    // next trial's independent Philox work into the FADD dependency chain.
+    template <int NT = 0>
+    PSA_DEV static R energy(const R* row, int n_rt, int) {
+        using V = Vec16<R>;
+        const int n = NT > 0 ? NT : n_rt;
         R acc[A];
 #pragma unroll
         for (int a = 0; a < A; ++a) acc[a] = Fam::init(a, n);
-        const R* p = V;
-#pragma unroll 4
-        for (int k = 0; k < n; ++k) {
+        const int m = n * A;
+        const int mv = m / V::W;
+        const typename V::T* p = reinterpret_cast<const typename V::T*>(row);
+        if constexpr (NT > 0) {
 #pragma unroll
-            for (int a = 0; a < A; ++a) acc[a] = fold<R>(Fam::op(a), acc[a], p[a * B]);
-            p += A * B;
+            for (int q = 0; q < (NT * A) / V::W; ++q) {
+                const typename V::T v = p[q];
+#pragma unroll
+                for (int i = 0; i < V::W; ++i) acc[i % A] = fold<R>(Fam::op(i % A), acc[i % A], V::get(v, i));
+            }
+#pragma unroll
+            for (int e = ((NT * A) / V::W) * V::W; e < NT * A; ++e)
+                acc[e % A] = fold<R>(Fam::op(e % A), acc[e % A], row[e]);
+        } else {
+#pragma unroll 5
+            for (int q = 0; q < mv; ++q) {
+                const typename V::T v = p[q];
+#pragma unroll
+                for (int i = 0; i < V::W; ++i) acc[i % A] = fold<R>(Fam::op(i % A), acc[i % A], V::get(v, i));
+            }
+            for (int e = mv * V::W; e < m; ++e) acc[e % A] = fold<R>(Fam::op(e % A), acc[e % A], row[e]);
         }
         return Fam::finish(acc, n);
     }
 };
 
 template <class R>
-struct ColumnX {
-    const R* V;
-    int B;
-    PSA_DEV R operator()(int k) const { return V[k * B]; }
+struct RowX {
+    const R* row;
+    PSA_DEV R operator()(int k) const { return row[k]; }
 };
 
 template <class R>
 struct FullCost {
     static constexpr int A = 1;
     PSA_DEV static void cache(R x, int, int, R* t) { t[0] = x; }
-    PSA_DEV static R energy(const R* V, int B, int n, int family) {
-        const ColumnX<R> x{V, B};
+    template <int NT = 0>
+    PSA_DEV static R energy(const R* row, int n, int family) {
+        const RowX<R> x{row};
         switch (family) {
         case PSA_FN_BRANIN: return Branin<R>::eval(x, n);
         case PSA_FN_DEKKERS_AARTS: return DekkersAarts<R>::eval(x, n);
@@ -85,20 +136,43 @@ struct FullCost {
 template <class R>
 struct Accept;
 
+// exact reference tests (sa_core.cpp:52-54)
 template <>
 struct Accept<double> {
-    PSA_DEV static bool test(double delta_e, double temperature, uint64_t m) {
+    PSA_DEV static bool exact(double delta_e, double temperature, uint64_t m) {
         return bits_to_uniform(m) <= libm::exp(-delta_e / temperature);
     }
 };
 
 template <>
 struct Accept<float> {
-    PSA_DEV static bool test(double delta_e, double temperature, uint64_t m) {
+    PSA_DEV static bool exact(double delta_e, double temperature, uint64_t m) {
         return bits_to_uniform_f32(m) <=
                libm::expf(-static_cast<float>(delta_e) / static_cast<float>(temperature));
     }
 };
+
+// The Metropolis decision with a fast, provably safe pre-test.  With
+// ya = -float(dE) * RN(1/float(T)) (relative error <= 3 ulp of float) and
+// e = __expf(ya) (MUFU.EX2-based), the exact exp(-dE/T) lies within a
+// factor (1 +- 2e-5) of e for every |ya| <= 40; a uniform more than 2^-12
+// (relative) below e is accepted and one above is rejected without the
+// exact test.  For ya < -40 the exact value is below 2^-53, the smallest
+// non-zero uniform, so only u == 0 (m == 0) accepts.  Everything else
+// (the ambiguous band, NaNs) takes the exact glibc-restated path, so the
+// decision is bit-identical to the reference for every input.
+template <class R>
+PSA_DEV bool metropolis_decide(double delta_e, double temperature, float inv_t, uint64_t m) {
+    if (delta_e <= 0) return true; // sa_core.cpp:50
+    const float ya = -static_cast<float>(delta_e) * inv_t;
+    const float uf = bits_to_uniform_f32(m);
+    const bool tiny = ya < -40.0f;
+    const float e = __expf(ya);
+    const bool sure_acc = tiny ? (m == 0) : (uf < e * (1.0f - 0x1p-12f));
+    const bool sure_rej = tiny ? (m != 0) : (uf > e * (1.0f + 0x1p-12f));
+    if (sure_acc | sure_rej) return sure_acc;
+    return Accept<R>::exact(delta_e, temperature, m);
+}
 
 // ---------------------------------------------------------------------------
 // Box description
@@ -124,44 +198,53 @@ struct SweepStats {
     uint64_t draws;
 };
 
-// V: this thread's column (V = base + threadIdx.x), stride B.
-// Returns the end energy; accept bits go to mask[w*mask_stride], w = j/32.
-// If x != nullptr (asynchronous engine), accepted coordinates are also
-// written to the double-precision point x[k*B] (stride B).
-template <class R, class Cost>
-PSA_DEV R sweep(R* V, int B, int n, int family, R E, double temperature, uint32_t chain,
-                uint32_t level, uint64_t ctr, int N, const Box& box, const PhiloxKeys& keys,
+// row: this thread's 16-byte aligned state row.  Returns the end energy;
+// accept bits go to mask[w*mask_stride], w = j/32.  If x != nullptr
+// (asynchronous engine), accepted coordinates are also written to the
+// double-precision point x[k] of this chain.
+//
+// The three draws of trial j+1 do not depend on trial j's outcome (the
+// streams are counter-based), so they are issued before the fold of trial j
+// and overlap its dependent FADD chain; the acceptance draw is therefore
+// computed even for downhill moves (it is consumed either way, rng.hpp).
+template <class R, class Cost, int NT = 0>
+PSA_DEV R sweep(R* row, int n_rt, int family, R E, double temperature, uint32_t chain,
+                uint32_t level, uint32_t ctr, int N, const Box& box, const PhiloxKeys& keys,
                 uint32_t* mask, size_t mask_stride, double* x, SweepStats& st) {
     constexpr int A = Cost::A;
+    const int n = NT > 0 ? NT : n_rt;
+    const float inv_t = 1.0f / static_cast<float>(temperature);
+    const PhiloxChain pc = philox_chain(chain, level, keys);
+    const double idx_scale = static_cast<double>(n) * 0x1.0p-53; // u*n == m*(n*2^-53) exactly
     uint32_t word = 0;
+    uint64_t m1 = draw_bits53_fast(ctr, pc, keys);
+    uint64_t m2 = draw_bits53_fast(ctr + 1, pc, keys);
     for (int j = 0; j < N; ++j) {
-        const uint64_t m1 = draw_bits53(ctr, chain, level, keys);
-        const int d = coordinate_index(bits_to_uniform(m1), n);
-        const uint64_t m2 = draw_bits53(ctr + 1, chain, level, keys);
+        const int d = min(static_cast<int>(static_cast<double>(m1) * idx_scale), n - 1);
         const double xnew = box.point(d, bits_to_uniform(m2));
         R tn[A], to[A];
         Cost::cache(static_cast<R>(xnew), d, n, tn);
-        R* slot = V + static_cast<size_t>(d) * A * B;
+        R* slot = row + d * A;
 #pragma unroll
         for (int a = 0; a < A; ++a) {
-            to[a] = slot[a * B];
-            slot[a * B] = tn[a];
+            to[a] = slot[a];
+            slot[a] = tn[a];
         }
-        const R trial = Cost::energy(V, B, n, family);
+        const uint64_t m3 = draw_bits53_fast(ctr + 2, pc, keys);
+        m1 = draw_bits53_fast(ctr + 3, pc, keys);
+        m2 = draw_bits53_fast(ctr + 4, pc, keys);
+        const R trial = Cost::template energy<NT>(row, n, family);
         const double delta_e = static_cast<double>(trial) - static_cast<double>(E);
-        bool acc = true;
-        if (!(delta_e <= 0)) {
-            const uint64_t m3 = draw_bits53(ctr + 2, chain, level, keys);
-            acc = Accept<R>::test(delta_e, temperature, m3);
-        }
+        // sa_core.cpp:46-55 (the acceptance draw is consumed either way)
+        const bool acc = metropolis_decide<R>(delta_e, temperature, inv_t, m3);
         ctr += 3;
         if (acc) {
             E = trial;
             word |= 1u << (j & 31);
-            if (x) x[static_cast<size_t>(d) * B] = xnew;
+            if (x) x[d] = xnew;
         } else {
 #pragma unroll
-            for (int a = 0; a < A; ++a) slot[a * B] = to[a];
+            for (int a = 0; a < A; ++a) slot[a] = to[a];
         }
         if ((j & 31) == 31 || j == N - 1) {
             if (mask) mask[static_cast<size_t>(j >> 5) * mask_stride] = word;

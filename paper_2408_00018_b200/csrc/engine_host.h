@@ -63,7 +63,7 @@ struct EngineKernels {
     size_t (*smem_eval)(int n, int B);
 };
 
-EngineKernels engine_kernels(int precision, int family);
+EngineKernels engine_kernels(int precision, int family, int n);
 const void* probe_uniforms_kernel();
 const void* probe_philox_kernel();
 const void* v1_finalize_kernel();
