@@ -219,6 +219,12 @@ psa_status psa_device_philox(const uint32_t* ctr, const uint32_t* key, int32_t c
 psa_status psa_device_evaluate(const psa_objective* f, int32_t precision, const double* x,
                                int32_t count, double* out);
 
+/* device copies of the glibc restatements (fn: 0 sinf, 1 cosf, 2 expf,
+ * 3/4/5 the branch-free hot-loop sqrtf/sinf/cosf with their validity flag in
+ * ok[i], 6 the compiler's sqrt.rn.f32) and of sin/cos/exp (fn 0/1/2) */
+psa_status psa_device_libm_f32(int32_t fn, const float* x, int32_t count, float* out, int32_t* ok);
+psa_status psa_device_libm_f64(int32_t fn, const double* x, int32_t count, double* out);
+
 /* ---- host restatements of glibc libm used by the device code ------------
  * The same __host__ __device__ source the kernels use, compiled for the host
  * so CPU tests can pin it against the system libm. */

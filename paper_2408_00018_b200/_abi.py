@@ -115,7 +115,7 @@ class psa_nm_result(C.Structure):
 
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG_DIR, "libparsa_b200.so")
+LIB_PATH = os.environ.get("PSA_LIB_PATH") or os.path.join(PKG_DIR, "libparsa_b200.so")
 
 _lib = None
 
@@ -151,6 +151,8 @@ def _declare(lib):
         "psa_libm_cos": (C.c_double, [C.c_double]),
         "psa_libm_exp": (C.c_double, [C.c_double]),
         "psa_plan_level_detail": (st, [C.c_void_p, P(C.c_int32), P(C.c_double), C.c_int32]),
+        "psa_device_libm_f32": (st, [C.c_int32, P(C.c_float), C.c_int32, P(C.c_float), P(C.c_int32)]),
+        "psa_device_libm_f64": (st, [C.c_int32, P(C.c_double), C.c_int32, P(C.c_double)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -168,7 +170,7 @@ EXPORTED_SYMBOLS = [
     "psa_hybrid_run", "psa_plan_create", "psa_plan_launch", "psa_plan_fetch", "psa_plan_info",
     "psa_plan_destroy", "psa_device_uniforms", "psa_device_philox", "psa_device_evaluate",
     "psa_libm_sinf", "psa_libm_cosf", "psa_libm_expf", "psa_libm_sin", "psa_libm_cos",
-    "psa_libm_exp", "psa_plan_level_detail",
+    "psa_libm_exp", "psa_plan_level_detail", "psa_device_libm_f32", "psa_device_libm_f64",
 ]
 
 

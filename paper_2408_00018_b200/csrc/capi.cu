@@ -544,6 +544,41 @@ psa_status psa_device_evaluate(const psa_objective* f, int32_t precision, const 
     });
 }
 
+psa_status psa_device_libm_f32(int32_t fn, const float* x, int32_t count, float* out, int32_t* ok) {
+    return guarded([&] {
+        require_device();
+        DevBuf<float> dx, dout;
+        DevBuf<int32_t> dok;
+        dx.alloc(count);
+        dout.alloc(count);
+        dok.alloc(count);
+        cuda_check(cudaMemcpy(dx.p, x, sizeof(float) * count, cudaMemcpyHostToDevice), "H2D");
+        int f = fn, c = count;
+        const float* xp = dx.p;
+        void* params[] = {&f, &xp, &c, &dout.p, &dok.p};
+        cuda_check(cudaLaunchKernel(psa::probe_libm_f32_kernel(), dim3(std::min(4096, (count + 255) / 256)), dim3(256),
+                                    params, 0, 0), "probe_libm_f32");
+        cuda_check(cudaMemcpy(out, dout.p, sizeof(float) * count, cudaMemcpyDeviceToHost), "D2H");
+        if (ok) cuda_check(cudaMemcpy(ok, dok.p, sizeof(int32_t) * count, cudaMemcpyDeviceToHost), "D2H");
+    });
+}
+
+psa_status psa_device_libm_f64(int32_t fn, const double* x, int32_t count, double* out) {
+    return guarded([&] {
+        require_device();
+        DevBuf<double> dx, dout;
+        dx.alloc(count);
+        dout.alloc(count);
+        cuda_check(cudaMemcpy(dx.p, x, sizeof(double) * count, cudaMemcpyHostToDevice), "H2D");
+        int f = fn, c = count;
+        const double* xp = dx.p;
+        void* params[] = {&f, &xp, &c, &dout.p};
+        cuda_check(cudaLaunchKernel(psa::probe_libm_f64_kernel(), dim3(std::min(4096, (count + 255) / 256)), dim3(256),
+                                    params, 0, 0), "probe_libm_f64");
+        cuda_check(cudaMemcpy(out, dout.p, sizeof(double) * count, cudaMemcpyDeviceToHost), "D2H");
+    });
+}
+
 float psa_libm_sinf(float x) { return psa::libm::sinf(x); }
 float psa_libm_cosf(float x) { return psa::libm::cosf(x); }
 float psa_libm_expf(float x) { return psa::libm::expf(x); }

@@ -28,6 +28,16 @@
 
 namespace cg = cooperative_groups;
 
+// Engine blocks never exceed 128 threads (capi.cu picks 128/64/32), and the
+// shared-memory chain state caps residency at about 4 such blocks per SM, so
+// the register budget can be 128 per thread without costing occupancy.
+#ifndef PSA_V2_MAX_THREADS
+#define PSA_V2_MAX_THREADS 128
+#endif
+#ifndef PSA_V2_MIN_BLOCKS
+#define PSA_V2_MIN_BLOCKS 4
+#endif
+
 namespace psa {
 
 // ---------------------------------------------------------------------------
@@ -142,7 +152,7 @@ __device__ void replay_winner(const EngineArgs& a, const Box& box, double* xs, i
 // ---------------------------------------------------------------------------
 
 template <class R, class Cost, int NT>
-__global__ void __launch_bounds__(256) v2_kernel(const EngineArgs a) {
+__global__ void __launch_bounds__(PSA_V2_MAX_THREADS, PSA_V2_MIN_BLOCKS) v2_kernel(const EngineArgs a) {
     constexpr int A = Cost::A;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     cg::grid_group grid = cg::this_grid();
@@ -448,6 +458,36 @@ __global__ void probe_philox(const uint32_t* ctr, uint32_t k0, uint32_t k1, int 
     }
 }
 
+// device libm restatements on caller points: fn 0 sinf, 1 cosf, 2 expf,
+// 3 sqrtf_common (ok ? value : NaN-flag), 4 sinf_common, 5 cosf_common,
+// 6 sqrt.rn.f32 (compiler intrinsic, reference for 3)
+__global__ void probe_libm_f32(int fn, const float* x, int count, float* out, int* ok_out) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < count; i += gridDim.x * blockDim.x) {
+        const float v = x[i];
+        bool ok = true;
+        float r;
+        switch (fn) {
+        case 0: r = libm::sinf(v); break;
+        case 1: r = libm::cosf(v); break;
+        case 2: r = libm::expf(v); break;
+        case 3: r = libm::sqrtf_common(v, ok); break;
+        case 4: r = libm::sinf_common(v, ok); break;
+        case 5: r = libm::cosf_common(v, ok); break;
+        default: r = __fsqrt_rn(v); break;
+        }
+        out[i] = r;
+        ok_out[i] = ok;
+    }
+}
+
+// device double libm restatements: fn 0 sin, 1 cos, 2 exp
+__global__ void probe_libm_f64(int fn, const double* x, int count, double* out) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < count; i += gridDim.x * blockDim.x) {
+        const double v = x[i];
+        out[i] = fn == 0 ? libm::sin(v) : fn == 1 ? libm::cos(v) : libm::exp(v);
+    }
+}
+
 // f(x_i) through the engine's own cache/energy path (one point per thread)
 template <class R, class Cost>
 __global__ void probe_evaluate(const EngineArgs a, const double* x, int count, double* out) {
@@ -499,6 +539,12 @@ EngineKernels sep_kernels(int n) {
 
 template <class R>
 EngineKernels kernels_for(int family, int n) {
+#ifdef PSA_EXPERIMENT_ONLY
+    // experiment builds: only the benchmark kernel (fast compile)
+    (void)family;
+    (void)n;
+    return KernelSet<R, SepCost<R, Schwefel>, 100>::get();
+#else
     switch (family) {
     case PSA_FN_SCHWEFEL: return sep_kernels<R, Schwefel>(n);
     case PSA_FN_ACKLEY: return KernelSet<R, SepCost<R, Ackley>>::get();
@@ -512,6 +558,7 @@ EngineKernels kernels_for(int family, int n) {
     case PSA_FN_SPHERE: return KernelSet<R, SepCost<R, Sphere>>::get();
     default: return KernelSet<R, FullCost<R>>::get();
     }
+#endif
 }
 
 EngineKernels engine_kernels(int precision, int family, int n) {
@@ -521,5 +568,7 @@ EngineKernels engine_kernels(int precision, int family, int n) {
 const void* probe_uniforms_kernel() { return reinterpret_cast<const void*>(&probe_uniforms); }
 const void* probe_philox_kernel() { return reinterpret_cast<const void*>(&probe_philox); }
 const void* v1_finalize_kernel() { return reinterpret_cast<const void*>(&v1_finalize); }
+const void* probe_libm_f32_kernel() { return reinterpret_cast<const void*>(&probe_libm_f32); }
+const void* probe_libm_f64_kernel() { return reinterpret_cast<const void*>(&probe_libm_f64); }
 
 } // namespace psa

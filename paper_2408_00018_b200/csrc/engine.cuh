@@ -54,12 +54,30 @@ struct Vec16<double> {
 // Cost interface
 // ---------------------------------------------------------------------------
 
+template <class F, class = void>
+struct HasCommon {
+    static constexpr bool value = false;
+};
+template <class F>
+struct HasCommon<F, decltype(void(F::kHasCommon))> {
+    static constexpr bool value = F::kHasCommon;
+};
+
 template <class R, template <class> class F>
 struct SepCost {
     using Fam = F<R>;
     static constexpr int A = Fam::kArrays;
     static_assert(Vec16<R>::W % A == 0, "array count must divide the vector width");
     PSA_DEV static void cache(R x, int k, int, R* t) { Fam::term(x, k, t); }
+    // branch-free cache for the hot loop when the family provides one
+    PSA_DEV static void cache_common(R x, int k, int n, R* t, bool& ok) {
+        if constexpr (HasCommon<Fam>::value) {
+            Fam::term_common(x, k, t, ok);
+        } else {
+            cache(x, k, n, t);
+            ok = true;
+        }
+    }
     // fold over a 16-byte aligned row, reference order k = 0..n-1 per array.
     // NT > 0: the dimension is a compile-time constant and the fold is one
     // straight-line block (no loop), so the scheduler can interleave the
@@ -75,12 +93,32 @@ struct SepCost {
         const int mv = m / V::W;
         const typename V::T* p = reinterpret_cast<const typename V::T*>(row);
         if constexpr (NT > 0) {
+            constexpr int NV = (NT * A) / V::W;
+#ifndef PSA_FOLD_PREFETCH
+#define PSA_FOLD_PREFETCH 4
+#endif
+#if PSA_FOLD_PREFETCH > 0
+            // loads run PSA_FOLD_PREFETCH vectors ahead of the FADD chain so
+            // the shared-memory latency stays hidden behind it
+            constexpr int PF = PSA_FOLD_PREFETCH < NV ? PSA_FOLD_PREFETCH : NV;
+            typename V::T buf[PF];
 #pragma unroll
-            for (int q = 0; q < (NT * A) / V::W; ++q) {
+            for (int q = 0; q < PF; ++q) buf[q] = p[q];
+#pragma unroll
+            for (int q = 0; q < NV; ++q) {
+                const typename V::T v = buf[q % PF];
+                if (q + PF < NV) buf[q % PF] = p[q + PF];
+#pragma unroll
+                for (int i = 0; i < V::W; ++i) acc[i % A] = fold<R>(Fam::op(i % A), acc[i % A], V::get(v, i));
+            }
+#else
+#pragma unroll
+            for (int q = 0; q < NV; ++q) {
                 const typename V::T v = p[q];
 #pragma unroll
                 for (int i = 0; i < V::W; ++i) acc[i % A] = fold<R>(Fam::op(i % A), acc[i % A], V::get(v, i));
             }
+#endif
 #pragma unroll
             for (int e = ((NT * A) / V::W) * V::W; e < NT * A; ++e)
                 acc[e % A] = fold<R>(Fam::op(e % A), acc[e % A], row[e]);
@@ -107,6 +145,10 @@ template <class R>
 struct FullCost {
     static constexpr int A = 1;
     PSA_DEV static void cache(R x, int, int, R* t) { t[0] = x; }
+    PSA_DEV static void cache_common(R x, int k, int n, R* t, bool& ok) {
+        cache(x, k, n, t);
+        ok = true;
+    }
     template <int NT = 0>
     PSA_DEV static R energy(const R* row, int n, int family) {
         const RowX<R> x{row};
@@ -217,23 +259,49 @@ PSA_DEV R sweep(R* row, int n_rt, int family, R E, double temperature, uint32_t 
     const PhiloxChain pc = philox_chain(chain, level, keys);
     const double idx_scale = static_cast<double>(n) * 0x1.0p-53; // u*n == m*(n*2^-53) exactly
     uint32_t word = 0;
-    uint64_t m1 = draw_bits53_fast(ctr, pc, keys);
-    uint64_t m2 = draw_bits53_fast(ctr + 1, pc, keys);
-    for (int j = 0; j < N; ++j) {
-        const int d = min(static_cast<int>(static_cast<double>(m1) * idx_scale), n - 1);
-        const double xnew = box.point(d, bits_to_uniform(m2));
-        R tn[A], to[A];
+    // trial 0's proposal; thereafter trial j+1's proposal (coordinate, value,
+    // new cached term) is built while trial j's fold runs
+    int d;
+    double xnew;
+    R tn[A];
+    {
+        const uint64_t m1 = draw_bits53_fast(ctr, pc, keys);
+        const uint64_t m2 = draw_bits53_fast(ctr + 1, pc, keys);
+        d = min(static_cast<int>(static_cast<double>(m1) * idx_scale), n - 1);
+        xnew = box.point(d, bits_to_uniform(m2));
         Cost::cache(static_cast<R>(xnew), d, n, tn);
+    }
+    for (int j = 0; j < N; ++j) {
+        R to[A];
         R* slot = row + d * A;
 #pragma unroll
         for (int a = 0; a < A; ++a) {
             to[a] = slot[a];
             slot[a] = tn[a];
         }
+        // independent of this trial's outcome: its acceptance draw and the
+        // next proposal (the streams are counter-based)
         const uint64_t m3 = draw_bits53_fast(ctr + 2, pc, keys);
-        m1 = draw_bits53_fast(ctr + 3, pc, keys);
-        m2 = draw_bits53_fast(ctr + 4, pc, keys);
+        const uint64_t m1 = draw_bits53_fast(ctr + 3, pc, keys);
+        const uint64_t m2 = draw_bits53_fast(ctr + 4, pc, keys);
+        const int dn = min(static_cast<int>(static_cast<double>(m1) * idx_scale), n - 1);
+        const double xn = box.point(dn, bits_to_uniform(m2));
+        R tnn[A];
+        bool ok;
+        Cost::cache_common(static_cast<R>(xn), dn, n, tnn, ok);
+#ifndef PSA_NO_PIN
+        // materialise them here so the scheduler interleaves them into the
+        // fold's FADD latency chain (left alone, the compiler sinks them)
+        asm volatile("" ::"l"(m3), "r"(dn));
+#pragma unroll
+        for (int a = 0; a < A; ++a) {
+            if constexpr (sizeof(R) == 4) asm volatile("" ::"f"(tnn[a]));
+            else asm volatile("" ::"d"(tnn[a]));
+        }
+#endif
         const R trial = Cost::template energy<NT>(row, n, family);
+        if (!ok) Cost::cache(static_cast<R>(xn), dn, n, tnn); // general path, practically never
+
         const double delta_e = static_cast<double>(trial) - static_cast<double>(E);
         // sa_core.cpp:46-55 (the acceptance draw is consumed either way)
         const bool acc = metropolis_decide<R>(delta_e, temperature, inv_t, m3);
@@ -250,6 +318,10 @@ PSA_DEV R sweep(R* row, int n_rt, int family, R E, double temperature, uint32_t 
             if (mask) mask[static_cast<size_t>(j >> 5) * mask_stride] = word;
             word = 0;
         }
+        d = dn;
+        xnew = xn;
+#pragma unroll
+        for (int a = 0; a < A; ++a) tn[a] = tnn[a];
     }
     st.evals += static_cast<uint64_t>(N);
     st.draws += 3ull * static_cast<uint64_t>(N);

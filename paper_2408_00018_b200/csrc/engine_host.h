@@ -67,5 +67,7 @@ EngineKernels engine_kernels(int precision, int family, int n);
 const void* probe_uniforms_kernel();
 const void* probe_philox_kernel();
 const void* v1_finalize_kernel();
+const void* probe_libm_f32_kernel();
+const void* probe_libm_f64_kernel();
 
 } // namespace psa

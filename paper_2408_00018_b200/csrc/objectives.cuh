@@ -148,7 +148,21 @@ template <class R>
 struct Schwefel {
     static constexpr bool kSeparable = true;
     static constexpr int kArrays = 1;
+    static constexpr bool kHasCommon = true;
     PSA_HD static void term(R x, int, R* t) { t[0] = x * Math<R>::sin(Math<R>::sqrt(Math<R>::fabs(x))); }
+    // branch-free common path (see libm_glibc.cuh); ok=false -> use term()
+    PSA_HD static void term_common(R x, int k, R* t, bool& ok) {
+        if constexpr (sizeof(R) == 4) {
+            bool ok1, ok2;
+            const float sq = libm::sqrtf_common(Math<float>::fabs(x), ok1);
+            const float sn = libm::sinf_common(sq, ok2);
+            t[0] = x * sn;
+            ok = ok1 & ok2;
+        } else {
+            term(x, k, t);
+            ok = true;
+        }
+    }
     PSA_HD static R init(int, int) { return R(0); }
     PSA_HD static int op(int) { return kAdd; }
     PSA_HD static R finish(const R* acc, int n) { return -acc[0] / R(n); }
