@@ -14,6 +14,7 @@
 #include <string.h>
 
 #include "parsa_suite_data.h"
+#include "parsa_stdsort.h"
 
 /* ------------------------------------------------------------------------ */
 /* RNG — rng.hpp                                                             */
@@ -598,22 +599,9 @@ int32_t orc_run_asynchronous(const psa_objective* f, const psa_engine_config* cf
 /* Nelder–Mead and hybrid — nelder_mead.cpp                                  */
 /* ------------------------------------------------------------------------ */
 
-typedef struct vertex {
-    double* x;
-    double f;
-} vertex;
-
-/* std::sort with operator< on f; a stable insertion sort gives the same
- * multiset order and an identical result whenever values are distinct
- * (ties among equal f values are not observable through the results). */
-static void sort_simplex(vertex* v, int m) {
-    for (int i = 1; i < m; ++i) {
-        vertex t = v[i];
-        int j = i - 1;
-        while (j >= 0 && t.f < v[j].f) { v[j + 1] = v[j]; --j; }
-        v[j + 1] = t;
-    }
-}
+/* The simplex as vertex ids: X[id*n + k], f[id]; pos[] is the physical
+ * order of std::vector<Vertex> simplex (nelder_mead.cpp:50), which
+ * std::sort permutes — restated exactly by psa_std_sort (libstdc++). */
 
 static double clampd(double v, double lo, double hi) { return v < lo ? lo : (hi < v ? hi : v); }
 
@@ -633,19 +621,21 @@ int32_t orc_nelder_mead_minimize(const psa_objective* f, const double* x_start,
     const int n = f->dim;
     uint64_t evals = 0;
 #define NM_EVAL(xx) (++evals, orc_evaluate(f->family, n, (xx)))
-    double* store = (double*)malloc(sizeof(double) * (size_t)(n + 1) * (size_t)n);
-    vertex* s = (vertex*)malloc(sizeof(vertex) * (size_t)(n + 1));
-    for (int i = 0; i <= n; ++i) s[i].x = store + (size_t)i * (size_t)n;
-    memcpy(s[0].x, x_start, sizeof(double) * (size_t)n);
-    s[0].f = NM_EVAL(s[0].x);
+    double* X = (double*)malloc(sizeof(double) * (size_t)(n + 1) * (size_t)n);
+    double* fv = (double*)malloc(sizeof(double) * (size_t)(n + 1));
+    int* pos = (int*)malloc(sizeof(int) * (size_t)(n + 1));
+#define VX(id) (X + (size_t)(id) * (size_t)n)
+    for (int v = 0; v <= n; ++v) pos[v] = v;
+    memcpy(VX(0), x_start, sizeof(double) * (size_t)n);
+    fv[0] = NM_EVAL(VX(0));
     for (int k = 0; k < n; ++k) { /* nelder_mead.cpp:52-58 */
-        memcpy(s[k + 1].x, x_start, sizeof(double) * (size_t)n);
+        double* x = VX(k + 1);
+        memcpy(x, x_start, sizeof(double) * (size_t)n);
         const double step = 0.05 * (f->upper[k] - f->lower[k]);
-        double* x = s[k + 1].x;
         x[k] = (x[k] + step <= f->upper[k]) ? x[k] + step : x[k] - step;
-        s[k + 1].f = NM_EVAL(x);
+        fv[k + 1] = NM_EVAL(x);
     }
-    sort_simplex(s, n + 1);
+    psa_std_sort(pos, n + 1, fv); /* :60 */
     double* cen = (double*)malloc(sizeof(double) * (size_t)n);
     double* xr = (double*)malloc(sizeof(double) * (size_t)n);
     double* xe = (double*)malloc(sizeof(double) * (size_t)n);
@@ -657,49 +647,55 @@ int32_t orc_nelder_mead_minimize(const psa_objective* f, const double* x_start,
         double diam = 0;
         for (int i = 1; i <= n; ++i)
             for (int k = 0; k < n; ++k) {
-                const double a = fabs(s[i].x[k] - s[0].x[k]);
+                const double a = fabs(VX(pos[i])[k] - VX(pos[0])[k]);
                 diam = diam < a ? a : diam; /* std::max(d, a) */
             }
-        if (s[n].f - s[0].f <= cfg->f_tol || diam <= cfg->x_tol) break;
+        if (fv[pos[n]] - fv[pos[0]] <= cfg->f_tol || diam <= cfg->x_tol) break;
         for (int k = 0; k < n; ++k) cen[k] = 0.0; /* :70-73 */
         for (int i = 0; i < n; ++i)
-            for (int k = 0; k < n; ++k) cen[k] += s[i].x[k] / n;
-        const double* worst = s[n].x;
-        const double worst_f = s[n].f;
+            for (int k = 0; k < n; ++k) cen[k] += VX(pos[i])[k] / n;
+        const int w = pos[n];
+        double* worst = VX(w);
+        const double worst_f = fv[w];
         for (int k = 0; k < n; ++k) xr[k] = clampd(cen[k] + cfg->reflect * (cen[k] - worst[k]), f->lower[k], f->upper[k]);
         const double fr = NM_EVAL(xr);
-        if (fr < s[0].f) {
+        if (fr < fv[pos[0]]) {
             for (int k = 0; k < n; ++k) xe[k] = clampd(cen[k] + cfg->expand * (xr[k] - cen[k]), f->lower[k], f->upper[k]);
             const double fe = NM_EVAL(xe);
-            if (fe < fr) { memcpy(s[n].x, xe, sizeof(double) * (size_t)n); s[n].f = fe; }
-            else { memcpy(s[n].x, xr, sizeof(double) * (size_t)n); s[n].f = fr; }
-        } else if (fr < s[n - 1].f) {
-            memcpy(s[n].x, xr, sizeof(double) * (size_t)n);
-            s[n].f = fr;
+            if (fe < fr) { memcpy(worst, xe, sizeof(double) * (size_t)n); fv[w] = fe; }
+            else { memcpy(worst, xr, sizeof(double) * (size_t)n); fv[w] = fr; }
+        } else if (fr < fv[pos[n - 1]]) {
+            memcpy(worst, xr, sizeof(double) * (size_t)n);
+            fv[w] = fr;
         } else {
             const int outside = fr < worst_f;
-            const double* toward = outside ? xr : worst;
-            for (int k = 0; k < n; ++k) xc[k] = clampd(cen[k] + cfg->contract * (toward[k] - cen[k]), f->lower[k], f->upper[k]);
+            for (int k = 0; k < n; ++k) {
+                const double toward = outside ? xr[k] : worst[k];
+                xc[k] = clampd(cen[k] + cfg->contract * (toward - cen[k]), f->lower[k], f->upper[k]);
+            }
             const double fc = NM_EVAL(xc);
             if (fc < (outside ? fr : worst_f)) {
-                memcpy(s[n].x, xc, sizeof(double) * (size_t)n);
-                s[n].f = fc;
+                memcpy(worst, xc, sizeof(double) * (size_t)n);
+                fv[w] = fc;
             } else {
+                const double* x0 = VX(pos[0]);
                 for (int i = 1; i <= n; ++i) {
+                    double* xi = VX(pos[i]);
                     for (int k = 0; k < n; ++k)
-                        s[i].x[k] = clampd(s[0].x[k] + cfg->shrink * (s[i].x[k] - s[0].x[k]), f->lower[k], f->upper[k]);
-                    s[i].f = NM_EVAL(s[i].x);
+                        xi[k] = clampd(x0[k] + cfg->shrink * (xi[k] - x0[k]), f->lower[k], f->upper[k]);
+                    fv[pos[i]] = NM_EVAL(xi);
                 }
             }
         }
-        sort_simplex(s, n + 1);
+        psa_std_sort(pos, n + 1, fv); /* :111 */
     }
 #undef NM_EVAL
-    if (out->x_best) memcpy(out->x_best, s[0].x, sizeof(double) * (size_t)n);
-    out->f_best = s[0].f;
+    if (out->x_best) memcpy(out->x_best, VX(pos[0]), sizeof(double) * (size_t)n);
+    out->f_best = fv[pos[0]];
     out->iterations = iter;
     out->evaluations = evals;
-    free(store); free(s); free(cen); free(xr); free(xe); free(xc);
+#undef VX
+    free(X); free(fv); free(pos); free(cen); free(xr); free(xe); free(xc);
     return 0;
 }
 

@@ -14,6 +14,8 @@ from .api import (  # noqa: F401
     InvalidArgument,
     LadderInfo,
     LogicError,
+    NelderMeadConfig,
+    NelderMeadResult,
     ObjectiveFunction,
     OutOfRange,
     PhaseBreakdown,
@@ -28,8 +30,10 @@ from .api import (  # noqa: F401
     evaluate_batch,
     evaluate_single,
     expected_evaluations,
+    hybrid_run,
     ladder,
     location_error,
+    nelder_mead_minimize,
     reduce_min,
     registry,
     registry_get,

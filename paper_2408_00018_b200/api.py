@@ -459,6 +459,67 @@ def run_synchronous(f: ObjectiveFunction, cfg: EngineConfig) -> RunResult:
 
 
 # ---------------------------------------------------------------------------
+# nelder_mead.hpp
+# ---------------------------------------------------------------------------
+
+@dataclass
+class NelderMeadConfig:
+    reflect: float = 1.0
+    expand: float = 2.0
+    contract: float = 0.5
+    shrink: float = 0.5
+    f_tol: float = 1e-12
+    x_tol: float = 1e-10
+    max_iters: int = 0  # 0 => 50000 * n
+
+    def effective_max_iters(self, n: int) -> int:
+        return self.max_iters if self.max_iters > 0 else 50000 * n
+
+    def _c(self):
+        return psa_nm_config(self.reflect, self.expand, self.contract, self.shrink, self.f_tol, self.x_tol,
+                             int(self.max_iters), 0)
+
+
+@dataclass
+class NelderMeadResult:
+    x_best: list
+    f_best: float
+    iterations: int
+    evaluations: int
+
+
+def nelder_mead_minimize(f: ObjectiveFunction, x_start: Sequence[float],
+                         cfg: Optional[NelderMeadConfig] = None) -> NelderMeadResult:
+    """nelder_mead.cpp:37-115, on the device (one cooperative block)."""
+    lib = _lib()
+    cfg = cfg or NelderMeadConfig()
+    h = _Objective(f)
+    x0 = np.ascontiguousarray(x_start, dtype=np.float64)
+    if len(x0) != f.dim:
+        raise InvalidArgument(f"contains: expected dimension {f.dim}, got {len(x0)}")
+    xb = np.zeros(f.dim)
+    r = psa_nm_result(xb.ctypes.data_as(C.POINTER(C.c_double)), 0.0, 0, 0, 0)
+    c = cfg._c()
+    _raise(lib, lib.psa_nelder_mead_minimize(C.byref(h.c), x0.ctypes.data_as(C.POINTER(C.c_double)),
+                                             C.byref(c), C.byref(r)))
+    return NelderMeadResult(xb.tolist(), r.f_best, r.iterations, r.evaluations)
+
+
+def hybrid_run(f: ObjectiveFunction, cfg: EngineConfig, truncated_sched: AnnealSchedule,
+               nm_cfg: Optional[NelderMeadConfig] = None) -> RunResult:
+    """nelder_mead.cpp:117-136: truncated synchronous SA, then the polish."""
+    lib = _lib()
+    nm_cfg = nm_cfg or NelderMeadConfig()
+    h = _Objective(f)
+    c = _Config(cfg)
+    r = _Result(f.dim, _levels_or_raise(truncated_sched) + 1)
+    ts = truncated_sched._c()
+    nm = nm_cfg._c()
+    _raise(lib, lib.psa_hybrid_run(C.byref(h.c), C.byref(c.c), C.byref(ts), C.byref(nm), C.byref(r.c)))
+    return r.to_run_result()
+
+
+# ---------------------------------------------------------------------------
 # device-resident plans (benchmarks, multi-GPU shards)
 # ---------------------------------------------------------------------------
 

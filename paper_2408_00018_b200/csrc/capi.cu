@@ -379,6 +379,68 @@ psa_status run_engine(const psa_objective* f, const psa_engine_config* cfg, int 
     });
 }
 
+// NelderMeadConfig::validate (nelder_mead.cpp:30-35)
+void validate_nm(const psa_nm_config& c) {
+    if (!(c.reflect > 0) || !(c.expand > 1) || !(c.contract > 0) || !(c.contract < 1) || !(c.shrink > 0) ||
+        !(c.shrink < 1))
+        fail(PSA_ERR_INVALID_ARGUMENT, "nelder-mead: coefficient out of range");
+}
+
+// nelder_mead_minimize (nelder_mead.cpp:37-115) on the device
+void nm_run(const psa_objective* f, const double* x_start, const psa_nm_config* nm, psa_nm_result* out,
+            cudaStream_t stream) {
+    if (!nm || !out || !x_start) fail(PSA_ERR_INVALID_ARGUMENT, "parsa_b200: null argument");
+    validate_nm(*nm);
+    check_objective(f);
+    const int n = f->dim;
+    for (int k = 0; k < n; ++k)
+        if (x_start[k] < f->lower[k] || x_start[k] > f->upper[k])
+            fail(PSA_ERR_INVALID_ARGUMENT, "nelder_mead_minimize: infeasible start");
+    require_device();
+    const int max_iters = nm->max_iters > 0 ? nm->max_iters : 50000 * n;
+    DevBuf<double> d_lo, d_hi, d_x0, d_X, d_xb;
+    DevBuf<psa::NMOut> d_out;
+    d_lo.alloc(n);
+    d_hi.alloc(n);
+    d_x0.alloc(n);
+    d_xb.alloc(n);
+    d_X.alloc(static_cast<size_t>(n + 1) * n);
+    d_out.alloc(1);
+    cuda_check(cudaMemcpy(d_lo.p, f->lower, sizeof(double) * n, cudaMemcpyHostToDevice), "H2D");
+    cuda_check(cudaMemcpy(d_hi.p, f->upper, sizeof(double) * n, cudaMemcpyHostToDevice), "H2D");
+    cuda_check(cudaMemcpy(d_x0.p, x_start, sizeof(double) * n, cudaMemcpyHostToDevice), "H2D");
+    psa::NMArgsHost a{};
+    a.n = n;
+    a.family = f->family;
+    a.max_iters = max_iters;
+    a.reflect = nm->reflect;
+    a.expand = nm->expand;
+    a.contract = nm->contract;
+    a.shrink = nm->shrink;
+    a.f_tol = nm->f_tol;
+    a.x_tol = nm->x_tol;
+    a.lower = d_lo.p;
+    a.upper = d_hi.p;
+    a.x_start = d_x0.p;
+    a.X = d_X.p;
+    a.x_best = d_xb.p;
+    a.out = d_out.p;
+    const void* k = psa::nm_kernel_for(f->family);
+    const size_t smem = psa::nm_smem_bytes(n);
+    cuda_check(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
+               "cudaFuncSetAttribute");
+    void* params[] = {&a};
+    cuda_check(cudaLaunchKernel(k, dim3(1), dim3(n >= 256 ? 512 : 128), params, smem, stream), "launch nm_kernel");
+    psa::NMOut o;
+    cuda_check(cudaMemcpyAsync(&o, d_out.p, sizeof(o), cudaMemcpyDeviceToHost, stream), "D2H");
+    if (out->x_best)
+        cuda_check(cudaMemcpyAsync(out->x_best, d_xb.p, sizeof(double) * n, cudaMemcpyDeviceToHost, stream), "D2H");
+    cuda_check(cudaStreamSynchronize(stream), "nm_kernel");
+    out->f_best = o.f_best;
+    out->iterations = o.iterations;
+    out->evaluations = o.evaluations;
+}
+
 } // namespace
 
 extern "C" {
@@ -430,15 +492,58 @@ psa_status psa_run_sequential(const psa_objective* f, const psa_engine_config* c
     return run_engine(f, cfg, 1, out);
 }
 
-psa_status psa_nelder_mead_minimize(const psa_objective*, const double*, const psa_nm_config*, psa_nm_result*) {
-    g_err = "parsa_b200: nelder_mead_minimize is not available in this build";
-    return PSA_ERR_LOGIC;
+psa_status psa_nelder_mead_minimize(const psa_objective* f, const double* x_start, const psa_nm_config* nm,
+                                    psa_nm_result* out) {
+    return guarded([&] { nm_run(f, x_start, nm, out, nullptr); });
 }
 
-psa_status psa_hybrid_run(const psa_objective*, const psa_engine_config*, const psa_schedule*,
-                          const psa_nm_config*, psa_run_result*) {
-    g_err = "parsa_b200: hybrid_run is not available in this build";
-    return PSA_ERR_LOGIC;
+psa_status psa_hybrid_run(const psa_objective* f, const psa_engine_config* cfg, const psa_schedule* truncated,
+                          const psa_nm_config* nm, psa_run_result* out) {
+    return guarded([&] {
+        const auto t0 = std::chrono::steady_clock::now();
+        if (!out || !cfg || !truncated || !nm) fail(PSA_ERR_INVALID_ARGUMENT, "parsa_b200: null argument");
+        psa_engine_config sa = *cfg; // nelder_mead.cpp:119-121
+        sa.schedule = *truncated;
+        {
+            psa_plan p;
+            plan_build(&p, f, &sa, 2, 0, sa.n_chains);
+            cudaStream_t s;
+            cuda_check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
+            try {
+                plan_launch(&p, s);
+                plan_fetch(&p, s, out);
+            } catch (...) {
+                cudaStreamDestroy(s);
+                throw;
+            }
+            cudaStreamDestroy(s);
+        }
+        out->wall_time_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        const double sa_best = out->best_f;
+        // nelder_mead.cpp:124-135
+        const auto t1 = std::chrono::steady_clock::now();
+        std::vector<double> xb(f->dim);
+        psa_nm_result r{xb.data(), 0, 0, 0, 0};
+        nm_run(f, out->best_x, nm, &r, nullptr);
+        out->wall_time_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - t1).count();
+        if (r.f_best <= out->best_f) {
+            out->best_f = r.f_best;
+            std::memcpy(out->best_x, xb.data(), sizeof(double) * f->dim);
+        }
+        out->has_phases = 1;
+        out->sa_evaluations = out->evaluations;
+        out->refine_evaluations = r.evaluations;
+        out->sa_best_f = sa_best;
+        out->evaluations += r.evaluations;
+        const int row = out->trace_len;
+        if (row < out->trace_capacity) {
+            out->trace[row].level = row;
+            out->trace[row].reserved = 0;
+            out->trace[row].cumulative_evals = out->evaluations;
+            out->trace[row].best_f = out->best_f;
+        }
+        out->trace_len = row + 1;
+    });
 }
 
 psa_status psa_plan_create(const psa_objective* f, const psa_engine_config* cfg, int32_t engine,

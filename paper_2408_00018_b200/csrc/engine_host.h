@@ -54,6 +54,27 @@ struct EngineArgs {
     OutScalars* out_scalars;
 };
 
+struct NMOut {
+    double f_best;
+    int32_t iterations;
+    int32_t pad;
+    unsigned long long evaluations;
+};
+
+struct NMArgsHost {
+    int n;
+    int family;
+    int max_iters;
+    int pad;
+    double reflect, expand, contract, shrink, f_tol, x_tol;
+    const double* lower;
+    const double* upper;
+    const double* x_start;
+    double* X;      // (n+1) x n simplex storage
+    double* x_best; // n
+    NMOut* out;
+};
+
 struct EngineKernels {
     const void* v2;
     const void* v1;
@@ -68,6 +89,8 @@ const void* probe_uniforms_kernel();
 const void* probe_philox_kernel();
 const void* v1_finalize_kernel();
 const void* probe_libm_f32_kernel();
+const void* nm_kernel_for(int family);
+size_t nm_smem_bytes(int n);
 const void* probe_libm_f64_kernel();
 
 } // namespace psa

@@ -154,6 +154,49 @@ def main():
         print(name, rec["best_f"], rec["winning_chain"], flush=True)
     out["runs"] = runs
 
+    # Nelder-Mead and hybrid (nelder_mead.cpp), default NelderMeadConfig
+    nm_default = (1.0, 2.0, 0.5, 0.5, 1e-12, 1e-10, 0)
+    nms = {}
+    for name, fam, dim, lo, hi, x0, iters in [
+            ("nm_sphere4", "SPHERE", 4, -2.048, 2.048, [1, 1, 1, 1], 0),
+            ("nm_rosenbrock4", "ROSENBROCK", 4, -2.048, 2.048, [0.5, 0.3, 0.1, 0.0], 0),
+            ("nm_shekel5", "SHEKEL5", 4, 0, 10, [4, 4, 4, 4], 0),
+            ("nm_schwefel8", "SCHWEFEL", 8, -512, 512, [400.0, 430.0, 415.0, 425.0, 410.0, 421.0, 419.0, 423.0], 0),
+            ("nm_griewank20", "GRIEWANK", 20, -600, 600, [3.0 * (k % 5 - 2) for k in range(20)], 2000),
+            ("nm_schwefel64_capped", "SCHWEFEL", 64, -512, 512, [420.0 + (k % 7) for k in range(64)], 3000)]:
+        prob = Problem(fam, dim, lo, hi)
+        x0a = np.array(x0, dtype=np.float64)
+        nmc = _abi.psa_nm_config(*nm_default[:6], iters, 0)
+        xb = np.zeros(dim)
+        r = _abi.psa_nm_result(xb.ctypes.data_as(C.POINTER(C.c_double)), 0, 0, 0, 0)
+        assert lib.ref_nelder_mead(C.byref(prob.c), x0a.ctypes.data_as(C.POINTER(C.c_double)), C.byref(nmc), C.byref(r)) == 0
+        nms[name] = {"family": fam, "dim": dim, "lo": lo, "hi": hi, "x0": [hx(v) for v in x0a], "max_iters": iters,
+                     "x_best": [hx(v) for v in xb], "f_best": hx(r.f_best), "iterations": r.iterations,
+                     "evaluations": r.evaluations}
+        print(name, r.f_best, r.iterations, flush=True)
+    out["nelder_mead"] = nms
+    hyb = {}
+    for name, fam, dim, lo, hi, chains, sch, trunc, seed in [
+            ("hybrid_rosenbrock4", "ROSENBROCK", 4, -2.048, 2.048, 64, (10, 1, 0.8, 10), (10, 0.5, 0.8, 10), 0),
+            ("hybrid_schwefel32", "SCHWEFEL", 32, -512, 512, 512, (100, 1, 0.9, 20), (100.0, 1.0, 0.9, 20), 1),
+            ("hybrid_griewank10", "GRIEWANK", 10, -600, 600, 256, (1000, 1, 0.9, 20), (1000.0, 1.0, 0.9, 20), 2)]:
+        prob = Problem(fam, dim, lo, hi)
+        cfg = Config(chains, sch, seed, 0, 0, workers=0)
+        ts = _abi.psa_schedule(*trunc, 0)
+        nmc = _abi.psa_nm_config(*nm_default[:6], 0, 0)
+        L = levels_of_cfg(Config(chains, trunc))
+        res = Result(dim, L + 2)
+        assert lib.ref_hybrid_run(C.byref(prob.c), C.byref(cfg.c), C.byref(ts), C.byref(nmc), C.byref(res.c)) == 0
+        d = res.as_dict()
+        hyb[name] = {"family": fam, "dim": dim, "lo": lo, "hi": hi, "chains": chains, "schedule": list(sch),
+                     "truncated": list(trunc), "seed": seed, "best_x": [hx(v) for v in d["best_x"]],
+                     "best_f": hx(d["best_f"]), "evaluations": d["evaluations"], "winning_chain": d["winning_chain"],
+                     "rng_draws": d["rng_draws"], "trace": [[a, b, hx(c)] for a, b, c in d["trace"]],
+                     "sa_evaluations": d["sa_evaluations"], "refine_evaluations": d["refine_evaluations"],
+                     "sa_best_f": hx(d["sa_best_f"])}
+        print(name, d["best_f"], d["refine_evaluations"], flush=True)
+    out["hybrid"] = hyb
+
     with open(os.path.join(HERE, "reference_golden.json"), "w") as fh:
         json.dump(out, fh, indent=1)
     print("wrote", os.path.join(HERE, "reference_golden.json"))

@@ -181,3 +181,43 @@ def test_error_messages_match_reference():
     assert ref_run(2, prob, cfg)["err"] == "schedule: need 0 < t_min < t0"
     cfg = Config(4, (5.0, 0.5, 0.7, 10))
     assert ref_run(0, prob, cfg)["err"] == "run_sequential: requires n_chains == 1"
+
+
+def _nm_cfg(max_iters=0):
+    from paper_2408_00018_b200._abi import psa_nm_config
+    return psa_nm_config(1.0, 2.0, 0.5, 0.5, 1e-12, 1e-10, max_iters, 0)
+
+
+@pytest.mark.parametrize("name", ["nm_sphere4", "nm_rosenbrock4", "nm_shekel5", "nm_schwefel8", "nm_griewank20",
+                                  "nm_schwefel64_capped"])
+def test_oracle_nelder_mead_bitwise(golden, name):
+    from paper_2408_00018_b200._abi import psa_nm_result
+    rec = golden["nelder_mead"][name]
+    prob = Problem(rec["family"], rec["dim"], rec["lo"], rec["hi"])
+    x0 = np.array([fx(h) for h in rec["x0"]])
+    xb = np.zeros(rec["dim"])
+    r = psa_nm_result(xb.ctypes.data_as(C.POINTER(C.c_double)), 0, 0, 0, 0)
+    cfg = _nm_cfg(rec["max_iters"])
+    assert oracle().orc_nelder_mead_minimize(C.byref(prob.c), x0.ctypes.data_as(C.POINTER(C.c_double)),
+                                            C.byref(cfg), C.byref(r)) == 0
+    assert [v.hex() for v in xb] == rec["x_best"]
+    assert r.f_best.hex() == rec["f_best"]
+    assert (r.iterations, r.evaluations) == (rec["iterations"], rec["evaluations"])
+
+
+@pytest.mark.parametrize("name", ["hybrid_rosenbrock4", "hybrid_schwefel32", "hybrid_griewank10"])
+def test_oracle_hybrid_bitwise(golden, name):
+    from paper_2408_00018_b200._abi import psa_schedule
+    rec = golden["hybrid"][name]
+    prob = Problem(rec["family"], rec["dim"], rec["lo"], rec["hi"])
+    cfg = Config(rec["chains"], tuple(rec["schedule"]), rec["seed"], 0, 0)
+    ts = psa_schedule(*rec["truncated"], 0)
+    L = levels_of_cfg(Config(rec["chains"], tuple(rec["truncated"])))
+    res = Result(rec["dim"], L + 2)
+    nm = _nm_cfg()
+    assert oracle().orc_hybrid_run(C.byref(prob.c), C.byref(cfg.c), C.byref(ts), C.byref(nm), C.byref(res.c)) == 0
+    d = res.as_dict()
+    assert [v.hex() for v in d["best_x"]] == rec["best_x"]
+    assert d["best_f"].hex() == rec["best_f"]
+    assert d["evaluations"] == rec["evaluations"] and d["refine_evaluations"] == rec["refine_evaluations"]
+    assert [[a, b, c.hex()] for a, b, c in d["trace"]] == rec["trace"]
