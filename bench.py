@@ -16,9 +16,10 @@ rho=0.99, N=100 (1146 levels), precision f32 (the paper's default).  One
   cpu_baseline  the reference's own CPU implementation (oracle/_ref, all host
              threads) on a bounded sample of the same workload
 
-Multi-GPU (torchrun, N>1): weak scaling, each rank runs an independent
-2^20-chain shard of the global chain range (global stream keys); the
-per-level minloc exchange is described in DESIGN.md.
+Multi-GPU (torchrun, N>1): weak scaling, 2^20 chains per GPU of one global
+synchronous run (global stream keys); the per-level minloc is exchanged
+inside the persistent kernel through peer-mapped mailboxes over NVLink
+(paper_2408_00018_b200/dist.py, engine.cu exchange_level).
 
 `--impl reference` runs only the reference CPU arm and prints its line.
 """
@@ -211,8 +212,12 @@ def main():
     sched = psa.AnnealSchedule(SCHEDULE[0], args.tmin, SCHEDULE[2], SCHEDULE[3])
     f = psa.registry_get("F0_a").with_dim(N_DIM)
     cfg = psa.EngineConfig(n_chains=total_chains, schedule=sched, precision=prec, seed=0)
-    begin, end = rank * chains_per_gpu, (rank + 1) * chains_per_gpu
-    plan = psa.Plan(f, cfg, engine=2, chain_begin=begin, chain_end=end)
+    if world > 1:
+        from paper_2408_00018_b200.dist import make_sharded_plan
+
+        plan = make_sharded_plan(f, cfg)  # peer-mailbox level exchange inside the kernel
+    else:
+        plan = psa.Plan(f, cfg, engine=2)
     levels = plan.levels
     evals_per_step_local = chains_per_gpu * (1 + SCHEDULE[3] * levels)
     evals_per_step = evals_per_step_local * world
@@ -265,7 +270,7 @@ def main():
         if world == 1:
             r = psa.run_synchronous(f, psa.EngineConfig(n_chains=chains_per_gpu, schedule=sched, precision=prec))
         else:
-            with psa.Plan(f, cfg, engine=2, chain_begin=begin, chain_end=end) as p2:
+            with make_sharded_plan(f, cfg) as p2:
                 p2.launch(sh)
                 r = p2.fetch(sh)
         torch.cuda.synchronize()
@@ -306,7 +311,8 @@ def main():
                    "schedule": {"t0": SCHEDULE[0], "t_min": args.tmin, "rho": SCHEDULE[2],
                                 "sweep_length": SCHEDULE[3], "levels": levels},
                    "evals_per_step": evals_per_step, "l2": "flushed (512 MB write) between timed steps",
-                   "parallelism": f"chains sharded over {world} GPU(s)"},
+                   "parallelism": f"chains sharded over {world} GPU(s), per-level minloc over NVLink peer mailboxes"
+                   if world > 1 else "1 GPU"},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "api": "psa_run_synchronous (C-ABI, host buffers)"},
         "gpu_launches": args.steps * plan.launches_per_run,

@@ -199,6 +199,29 @@ psa_status psa_plan_fetch(psa_plan* p, void* cuda_stream, psa_run_result* out);
 psa_status psa_plan_info(const psa_plan* p, int32_t* levels, int32_t* chains,
                          int32_t* launches_per_run);
 psa_status psa_plan_destroy(psa_plan* p);
+/* Multi-GPU: a plan may be one rank of a `world`-GPU synchronous run.  Each
+ * rank owns a mailbox in its device memory; every rank maps every peer's
+ * mailbox (CUDA IPC across processes, or plain pointers within one process)
+ * and the persistent kernel exchanges the per-level minloc record through
+ * them (engine.cu: exchange_level).  max_blocks > 0 caps the grid (lets
+ * several cooperative plans share one GPU). */
+typedef struct psa_plan_options {
+    int32_t max_blocks;
+    int32_t rank;
+    int32_t world;
+    int32_t reserved;
+} psa_plan_options;
+psa_status psa_plan_create_ex(const psa_objective* f, const psa_engine_config* cfg, int32_t engine,
+                              int32_t chain_begin, int32_t chain_end, const psa_plan_options* opt,
+                              psa_plan** out);
+psa_status psa_plan_mailbox(const psa_plan* p, void** dev_ptr, uint64_t* bytes);
+/* 64-byte cudaIpcMemHandle_t of the plan's mailbox */
+psa_status psa_plan_mailbox_ipc_handle(const psa_plan* p, void* handle);
+psa_status psa_ipc_open(const void* handle, void** dev_ptr);
+psa_status psa_ipc_close(void* dev_ptr);
+/* mailboxes[r] = rank r's mailbox as addressable from this device; must be
+ * called before the first launch of a world > 1 plan */
+psa_status psa_plan_set_peers(psa_plan* p, void* const* mailboxes, int32_t world);
 /* synchronous plans: per-level winner chain and its end energy (diagnostic,
  * engines.cpp:187-192), copied to caller buffers of `capacity` entries */
 psa_status psa_plan_level_detail(const psa_plan* p, int32_t* winners, double* winner_f,

@@ -104,6 +104,15 @@ class psa_nm_config(C.Structure):
     ]
 
 
+class psa_plan_options(C.Structure):
+    _fields_ = [
+        ("max_blocks", C.c_int32),
+        ("rank", C.c_int32),
+        ("world", C.c_int32),
+        ("reserved", C.c_int32),
+    ]
+
+
 class psa_nm_result(C.Structure):
     _fields_ = [
         ("x_best", C.POINTER(C.c_double)),
@@ -153,6 +162,13 @@ def _declare(lib):
         "psa_plan_level_detail": (st, [C.c_void_p, P(C.c_int32), P(C.c_double), C.c_int32]),
         "psa_device_libm_f32": (st, [C.c_int32, P(C.c_float), C.c_int32, P(C.c_float), P(C.c_int32)]),
         "psa_device_libm_f64": (st, [C.c_int32, P(C.c_double), C.c_int32, P(C.c_double)]),
+        "psa_plan_create_ex": (st, [P(psa_objective), P(psa_engine_config), C.c_int32, C.c_int32, C.c_int32,
+                                    P(psa_plan_options), P(C.c_void_p)]),
+        "psa_plan_mailbox": (st, [C.c_void_p, P(C.c_void_p), P(C.c_uint64)]),
+        "psa_plan_mailbox_ipc_handle": (st, [C.c_void_p, C.c_void_p]),
+        "psa_ipc_open": (st, [C.c_void_p, P(C.c_void_p)]),
+        "psa_ipc_close": (st, [C.c_void_p]),
+        "psa_plan_set_peers": (st, [C.c_void_p, P(C.c_void_p), C.c_int32]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -171,6 +187,8 @@ EXPORTED_SYMBOLS = [
     "psa_plan_destroy", "psa_device_uniforms", "psa_device_philox", "psa_device_evaluate",
     "psa_libm_sinf", "psa_libm_cosf", "psa_libm_expf", "psa_libm_sin", "psa_libm_cos",
     "psa_libm_exp", "psa_plan_level_detail", "psa_device_libm_f32", "psa_device_libm_f64",
+    "psa_plan_create_ex", "psa_plan_mailbox", "psa_plan_mailbox_ipc_handle", "psa_ipc_open",
+    "psa_ipc_close", "psa_plan_set_peers",
 ]
 
 

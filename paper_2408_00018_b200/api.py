@@ -526,23 +526,51 @@ def hybrid_run(f: ObjectiveFunction, cfg: EngineConfig, truncated_sched: AnnealS
 class Plan:
     """A device-resident engine run: upload once, launch many times on a
     caller-supplied CUDA stream (`stream` is an int cudaStream_t handle, e.g.
-    torch.cuda.current_stream().cuda_stream), fetch the RunResult."""
+    torch.cuda.current_stream().cuda_stream), fetch the RunResult.
+
+    `rank`/`world` make the plan one shard of a multi-GPU synchronous run
+    (chains [chain_begin, chain_end) of the global range); connect the ranks'
+    mailboxes with `set_peers` before the first launch (see dist.py)."""
 
     def __init__(self, f: ObjectiveFunction, cfg: EngineConfig, engine: int = 2,
-                 chain_begin: int = 0, chain_end: Optional[int] = None):
+                 chain_begin: int = 0, chain_end: Optional[int] = None,
+                 rank: int = 0, world: int = 1, max_blocks: int = 0):
         self._lib = _lib()
         self._h = _Objective(f)
         self._c = _Config(cfg)
         self.f = f
         self.cfg = cfg
+        self.rank, self.world = rank, world
         end = cfg.n_chains if chain_end is None else chain_end
         p = C.c_void_p()
-        _raise(self._lib, self._lib.psa_plan_create(C.byref(self._h.c), C.byref(self._c.c), int(engine),
-                                                    int(chain_begin), int(end), C.byref(p)))
+        opt = _abi.psa_plan_options(int(max_blocks), int(rank), int(world), 0)
+        _raise(self._lib, self._lib.psa_plan_create_ex(C.byref(self._h.c), C.byref(self._c.c), int(engine),
+                                                       int(chain_begin), int(end), C.byref(opt), C.byref(p)))
         self._p = p
         lv, ch, la = C.c_int32(), C.c_int32(), C.c_int32()
         _raise(self._lib, self._lib.psa_plan_info(p, C.byref(lv), C.byref(ch), C.byref(la)))
         self.levels, self.chains, self.launches_per_run = lv.value, ch.value, la.value
+        self._opened = []
+
+    def mailbox(self) -> int:
+        ptr = C.c_void_p()
+        _raise(self._lib, self._lib.psa_plan_mailbox(self._p, C.byref(ptr), None))
+        return ptr.value
+
+    def mailbox_ipc_handle(self) -> bytes:
+        buf = (C.c_char * 64)()
+        _raise(self._lib, self._lib.psa_plan_mailbox_ipc_handle(self._p, buf))
+        return bytes(buf)
+
+    def open_ipc(self, handle: bytes) -> int:
+        ptr = C.c_void_p()
+        _raise(self._lib, self._lib.psa_ipc_open(C.create_string_buffer(handle, 64), C.byref(ptr)))
+        self._opened.append(ptr.value)
+        return ptr.value
+
+    def set_peers(self, mailboxes):
+        arr = (C.c_void_p * len(mailboxes))(*mailboxes)
+        _raise(self._lib, self._lib.psa_plan_set_peers(self._p, arr, len(mailboxes)))
 
     def launch(self, stream: int = 0):
         _raise(self._lib, self._lib.psa_plan_launch(self._p, C.c_void_p(stream)))
@@ -560,6 +588,9 @@ class Plan:
         return w, e
 
     def close(self):
+        for ptr in getattr(self, "_opened", []):
+            self._lib.psa_ipc_close(C.c_void_p(ptr))
+        self._opened = []
         if self._p:
             self._lib.psa_plan_destroy(self._p)
             self._p = None

@@ -189,12 +189,28 @@ struct psa_plan {
     DevBuf<Cand> d_cand, d_cand_start, d_trace_cand;
     DevBuf<OutScalars> d_out;
     uint64_t expected_evals = 0, expected_draws = 0;
+    // multi-GPU exchange
+    int world = 1, rank = 0, max_blocks = 0;
+    unsigned epoch = 0;
+    bool peers_set = false;
+    DevBuf<char> d_mail;
+    DevBuf<char*> d_peers;
+    DevBuf<int> d_error;
+    size_t rec_stride = 0;
 };
 
 namespace {
 
 void plan_build(psa_plan* p, const psa_objective* f, const psa_engine_config* cfg, int engine,
-                int32_t chain_begin, int32_t chain_end) {
+                int32_t chain_begin, int32_t chain_end, const psa_plan_options* opt = nullptr) {
+    if (opt) {
+        p->world = opt->world > 0 ? opt->world : 1;
+        p->rank = opt->rank;
+        p->max_blocks = opt->max_blocks;
+        if (p->rank < 0 || p->rank >= p->world) fail(PSA_ERR_INVALID_ARGUMENT, "parsa_b200: rank out of range");
+        if (p->world > 1 && engine != 2)
+            fail(PSA_ERR_INVALID_ARGUMENT, "parsa_b200: multi-GPU exchange needs the synchronous engine");
+    }
     const char* who = engine == 1 ? "run_asynchronous" : "run_synchronous";
     validate_schedule(cfg->schedule); // engines.cpp:133
     if (cfg->n_chains < 1) fail(PSA_ERR_INVALID_ARGUMENT, std::string(who) + ": need n_chains >= 1");
@@ -246,6 +262,7 @@ void plan_build(psa_plan* p, const psa_objective* f, const psa_engine_config* cf
     if (per_sm < 1) fail(PSA_ERR_CUDA, "parsa_b200: engine kernel cannot be resident");
     const long long need = (static_cast<long long>(p->chains_local) + B - 1) / B;
     p->grid = static_cast<int>(std::min<long long>(need, static_cast<long long>(per_sm) * prop.multiProcessorCount));
+    if (p->max_blocks > 0) p->grid = std::min(p->grid, p->max_blocks);
 
     // device buffers
     p->d_lower.alloc(n);
@@ -299,6 +316,21 @@ void plan_build(psa_plan* p, const psa_objective* f, const psa_engine_config* cf
     a.level_winner = p->d_winner.p;
     a.level_winner_f = p->d_winner_f.p;
     a.out_scalars = p->d_out.p;
+    p->d_error.alloc(1);
+    cuda_check(cudaMemset(p->d_error.p, 0, sizeof(int)), "memset");
+    a.error_flag = p->d_error.p;
+    a.world = p->world;
+    a.rank = p->rank;
+    a.spin_limit = 60ll * 2000000000ll; // ~60 s at 2 GHz
+    if (p->world > 1) {
+        p->rec_stride = (48 + sizeof(double) * static_cast<size_t>(n) + 127) & ~size_t(127);
+        p->d_mail.alloc(2 * static_cast<size_t>(p->world) * p->rec_stride);
+        cuda_check(cudaMemset(p->d_mail.p, 0, 2 * static_cast<size_t>(p->world) * p->rec_stride), "memset");
+        p->d_peers.alloc(p->world);
+        a.rec_stride = p->rec_stride;
+        a.mail_self = p->d_mail.p;
+        a.mail_peers = p->d_peers.p;
+    }
 
     // the device keeps per-stream draw counters in 32 bits (philox.cuh)
     const uint64_t max_draw = static_cast<uint64_t>(n) + 3ull * p->N * (engine == 1 ? p->levels : 1) + 8;
@@ -313,7 +345,10 @@ void plan_build(psa_plan* p, const psa_objective* f, const psa_engine_config* cf
 }
 
 void plan_launch(psa_plan* p, cudaStream_t s) {
+    if (p->world > 1 && !p->peers_set)
+        fail(PSA_ERR_INVALID_ARGUMENT, "parsa_b200: multi-GPU plan launched before psa_plan_set_peers");
     cuda_check(cudaMemsetAsync(p->d_out.p, 0, sizeof(OutScalars), s), "memset");
+    p->args.epoch = ++p->epoch; // mailbox records of this launch carry the epoch
     void* params[] = {&p->args};
     if (p->engine == 2) {
         cuda_check(cudaLaunchCooperativeKernel(p->ks.v2, dim3(p->grid), dim3(p->block), params, p->smem, s),
@@ -335,7 +370,10 @@ void plan_fetch(psa_plan* p, cudaStream_t s, psa_run_result* out) {
     cuda_check(cudaMemcpyAsync(trace.data(), p->d_trace.p, sizeof(double) * p->levels, cudaMemcpyDeviceToHost, s), "D2H");
     if (out->best_x)
         cuda_check(cudaMemcpyAsync(out->best_x, p->d_bestx.p, sizeof(double) * p->n, cudaMemcpyDeviceToHost, s), "D2H");
+    int err_flag = 0;
+    cuda_check(cudaMemcpyAsync(&err_flag, p->d_error.p, sizeof(int), cudaMemcpyDeviceToHost, s), "D2H");
     cuda_check(cudaStreamSynchronize(s), "engine run");
+    if (err_flag) fail(PSA_ERR_CUDA, "parsa_b200: multi-GPU level exchange timed out (a peer never published)");
     // accounting cross-check (harness.cpp:148-155): the device counted every trial
     if (o.evaluations != p->expected_evals || o.rng_draws != p->expected_draws) {
         std::ostringstream m;
@@ -352,8 +390,10 @@ void plan_fetch(psa_plan* p, cudaStream_t s, psa_run_result* out) {
     for (int l = 0; l < p->levels && l < out->trace_capacity; ++l) {
         out->trace[l].level = l;
         out->trace[l].reserved = 0;
+        // engines.cpp:48-51, over the global chain count (a shard reports the
+        // global trace; evaluations/rng_draws above are the shard's own)
         out->trace[l].cumulative_evals =
-            static_cast<uint64_t>(p->chains_local) * (1 + static_cast<uint64_t>(p->N) * (l + 1));
+            static_cast<uint64_t>(p->chains_total) * (1 + static_cast<uint64_t>(p->N) * (l + 1));
         out->trace[l].best_f = trace[l];
     }
 }
@@ -558,6 +598,63 @@ psa_status psa_plan_create(const psa_objective* f, const psa_engine_config* cfg,
             throw;
         }
         *out = p;
+    });
+}
+
+psa_status psa_plan_create_ex(const psa_objective* f, const psa_engine_config* cfg, int32_t engine,
+                              int32_t chain_begin, int32_t chain_end, const psa_plan_options* opt,
+                              psa_plan** out) {
+    return guarded([&] {
+        if (engine != 1 && engine != 2) fail(PSA_ERR_INVALID_ARGUMENT, "parsa_b200: engine must be 1 or 2");
+        auto* p = new psa_plan;
+        try {
+            plan_build(p, f, cfg, engine, chain_begin, chain_end, opt);
+        } catch (...) {
+            delete p;
+            throw;
+        }
+        *out = p;
+    });
+}
+
+psa_status psa_plan_mailbox(const psa_plan* p, void** dev_ptr, uint64_t* bytes) {
+    return guarded([&] {
+        if (p->world < 2) fail(PSA_ERR_INVALID_ARGUMENT, "parsa_b200: plan has no mailbox (world == 1)");
+        *dev_ptr = p->d_mail.p;
+        if (bytes) *bytes = p->d_mail.n;
+    });
+}
+
+psa_status psa_plan_mailbox_ipc_handle(const psa_plan* p, void* handle) {
+    return guarded([&] {
+        if (p->world < 2) fail(PSA_ERR_INVALID_ARGUMENT, "parsa_b200: plan has no mailbox (world == 1)");
+        cudaIpcMemHandle_t h;
+        cuda_check(cudaIpcGetMemHandle(&h, p->d_mail.p), "cudaIpcGetMemHandle");
+        std::memcpy(handle, &h, sizeof(h));
+    });
+}
+
+psa_status psa_ipc_open(const void* handle, void** dev_ptr) {
+    return guarded([&] {
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, handle, sizeof(h));
+        cuda_check(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+    });
+}
+
+psa_status psa_ipc_close(void* dev_ptr) {
+    return guarded([&] { cuda_check(cudaIpcCloseMemHandle(dev_ptr), "cudaIpcCloseMemHandle"); });
+}
+
+psa_status psa_plan_set_peers(psa_plan* p, void* const* mailboxes, int32_t world) {
+    return guarded([&] {
+        if (world != p->world) fail(PSA_ERR_INVALID_ARGUMENT, "parsa_b200: peer count does not match the plan");
+        std::vector<char*> v(world);
+        for (int i = 0; i < world; ++i) v[i] = static_cast<char*>(mailboxes[i]);
+        if (v[p->rank] != p->d_mail.p)
+            fail(PSA_ERR_INVALID_ARGUMENT, "parsa_b200: peers[rank] must be the plan's own mailbox");
+        cuda_check(cudaMemcpy(p->d_peers.p, v.data(), sizeof(char*) * world, cudaMemcpyHostToDevice), "H2D");
+        p->peers_set = true;
     });
 }
 

@@ -148,6 +148,92 @@ __device__ void replay_winner(const EngineArgs& a, const Box& box, double* xs, i
 }
 
 // ---------------------------------------------------------------------------
+// Multi-GPU level minloc over peer memory (NVLink / NVSwitch)
+//
+// Every GPU owns a mailbox of 2 (level parity) x world records; a record is
+// {seq, e, c, es, cs, x[n]}: the GPU's level winner (energy, global chain),
+// its start-scan winner (level 0, random starts) and the winner's end point
+// rebuilt by replay_winner.  Block 0 of each GPU stores its record into
+// every peer's mailbox (plain stores through the peer mapping, then a
+// system-scope fence and a release store of seq = epoch:level+1); every block
+// of every GPU then acquires all `world` records of the level from its own
+// mailbox and runs the same deterministic selection (better(): energy, then
+// smallest global chain), so all GPUs continue from the same x* bit for bit.
+// Parity double-buffering is safe for the same reason as cand[]: a GPU can
+// only publish level l+2 after every GPU has published level l+1, which each
+// does only after it has finished reading level l.
+// ---------------------------------------------------------------------------
+
+struct MailHeader {
+    unsigned long long seq;
+    double e;
+    int32_t c;
+    int32_t pad0;
+    double es;
+    int32_t cs;
+    int32_t pad1;
+};
+constexpr size_t kMailHeaderBytes = 48;
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ void exchange_level(const EngineArgs& a, double* xs, Cand& w, Cand& ws, int l, Cand* scratch) {
+    const int n = a.n, tid = threadIdx.x, B = blockDim.x;
+    const size_t slot0 = static_cast<size_t>(l & 1) * a.world;
+    const unsigned long long tag = (static_cast<unsigned long long>(a.epoch) << 32) | static_cast<unsigned>(l + 1);
+    if (blockIdx.x == 0) {
+        for (int p = 0; p < a.world; ++p) {
+            char* rec = a.mail_peers[p] + (slot0 + a.rank) * a.rec_stride;
+            double* rx = reinterpret_cast<double*>(rec + kMailHeaderBytes);
+            for (int k = tid; k < n; k += B) rx[k] = xs[k];
+            if (tid == 0) {
+                MailHeader* h = reinterpret_cast<MailHeader*>(rec);
+                h->e = w.e;
+                h->c = w.c;
+                h->es = ws.e;
+                h->cs = ws.c;
+            }
+        }
+        __threadfence_system();
+        __syncthreads();
+        if (tid == 0)
+            for (int p = 0; p < a.world; ++p)
+                st_release_sys(reinterpret_cast<unsigned long long*>(a.mail_peers[p] + (slot0 + a.rank) * a.rec_stride),
+                               tag);
+    }
+    // acquire the level's records from this GPU's own mailbox
+    Cand g = empty_cand(), gs = empty_cand();
+    if (tid < a.world) {
+        const char* rec = a.mail_self + (slot0 + tid) * a.rec_stride;
+        const long long t0 = clock64();
+        while (ld_acquire_sys(reinterpret_cast<const unsigned long long*>(rec)) != tag) {
+            if (clock64() - t0 > a.spin_limit) {
+                atomicExch(a.error_flag, 1); // a peer never arrived: report instead of hanging
+                break;
+            }
+        }
+        const volatile MailHeader* h = reinterpret_cast<const volatile MailHeader*>(rec);
+        g = Cand{h->e, h->c, tid};
+        gs = Cand{h->es, h->cs, tid};
+    }
+    g = block_argmin(g, scratch);
+    if (l == 0 && a.random_start) gs = block_argmin(gs, scratch);
+    const volatile double* rx =
+        reinterpret_cast<const volatile double*>(a.mail_self + (slot0 + g.aux) * a.rec_stride + kMailHeaderBytes);
+    for (int k = tid; k < n; k += B) xs[k] = rx[k];
+    __syncthreads();
+    w = g;
+    if (l == 0 && a.random_start) ws = gs;
+}
+
+// ---------------------------------------------------------------------------
 // V2 persistent kernel
 // ---------------------------------------------------------------------------
 
@@ -257,6 +343,7 @@ __global__ void __launch_bounds__(PSA_V2_MAX_THREADS, PSA_V2_MIN_BLOCKS) v2_kern
         __syncthreads();
         replay_winner(a, box, xs, l, w.c, masks);
         __syncthreads();
+        if (a.world > 1) exchange_level(a, xs, w, ws, l, scratch); // the multi-GPU minloc
         cache_point<R, Cost>(xs, vs, n, a.family);
         if (tid == 0) sh->estar = w.e;
         __syncthreads();

@@ -52,6 +52,15 @@ struct EngineArgs {
     int32_t* level_winner; // V2: [levels] (diagnostic)
     double* level_winner_f;
     OutScalars* out_scalars;
+    // multi-GPU level exchange (world > 1): peer-mapped mailboxes
+    int world;
+    int rank;
+    unsigned epoch;         // launch counter, tags mailbox records
+    size_t rec_stride;      // bytes per mailbox record
+    char* mail_self;        // this GPU's mailbox [2][world] records
+    char* const* mail_peers; // device array: every GPU's mailbox as seen from here
+    long long spin_limit;   // clock64 cycles before a missing peer is reported
+    int* error_flag;
 };
 
 struct NMOut {

@@ -30,13 +30,19 @@ __global__ void __launch_bounds__(512) smem_bw(float* out, int iters) {
     for (int i = t; i < 4096; i += blockDim.x) buf[i] = make_float4(i, i + 1, i + 2, i + 3);
     __syncthreads();
     float4 acc = make_float4(0, 0, 0, 0);
-    // each thread walks its own row of 64 vectors (stride 4 mod 8 words -> conflict-free)
-    const float4* row = buf + (t % 64) * 17 % 4096;
+    // a warp reads 32 consecutive 16-byte vectors per instruction (4
+    // conflict-free wavefronts); the address changes every iteration and the
+    // loads are volatile so none can be hoisted or merged
+    const unsigned base = static_cast<unsigned>(__cvta_generic_to_shared(buf));
 #pragma unroll 1
     for (int it = 0; it < iters; ++it) {
 #pragma unroll
         for (int q = 0; q < 16; ++q) {
-            const float4 v = row[(q * 65) & 1023];
+            const unsigned idx = (t + 32 * q + 512 * it) & 4095;
+            float4 v;
+            asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+                         : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                         : "r"(base + 16 * idx));
             acc.x += v.x;
             acc.y += v.y;
             acc.z += v.z;
