@@ -284,21 +284,36 @@ def main():
     h2d = 8 * (3 * N_DIM + levels) + 256  # bounds, widths, start, ladder, kernel args
     d2h = 8 * (N_DIM + levels) + 32       # best_x, trace, scalars
 
-    # roofline of the engine kernel: SM issue roofline
+    # Roofline of the engine kernel ("Roofline"): the binding
+    # resource of the term-cached sweep is shared-memory bandwidth — every
+    # trial's sequential fold must read the chain's n cached terms (4n bytes
+    # in f32, 8n in f64) from its shared-memory row.  Peak: the LDS.128
+    # bandwidth measured on this pool's B200 by scripts/simt_peaks.cu.
     sm_count = torch.cuda.get_device_properties(local).multi_processor_count
     peaks_path = os.path.join(ROOT, "profiles", "simt_peaks.json")
-    peak_src = "nominal"
-    issue_peak = sm_count * 128 * 1.965e9  # lane-ops/s at max clock
+    smem_peak = sm_count * 128 * 1.965e9  # nominal 128 B/clk/SM at max clock
+    peak_src = "nominal 128 B/clk/SM x 148 SMs x 1.965 GHz"
     if os.path.exists(peaks_path):
         try:
-            pk = json.load(open(peaks_path))
-            issue_peak = float(pk["fp32_lane_ops_per_s"])
-            peak_src = "measured (profiles/simt_peaks.json)"
+            smem_peak = float(json.load(open(peaks_path))["smem_bytes_per_s"])
+            peak_src = "measured: profiles/simt_peaks.json (scripts/simt_peaks.cu, LDS.128 stream)"
         except (OSError, KeyError, ValueError):
             pass
-    ops_per_trial = 2 * N_DIM + 3 * 40 + 40  # fold (LDS+FADD per term) + 3 Philox + new term/accept
+    term_bytes = (4 if args.precision == "f32" else 8) * N_DIM
     trials_local = chains_per_gpu * SCHEDULE[3] * levels
-    achieved_ops = trials_local * ops_per_trial / (local_ms / args.steps / 1e3)
+    kernel_s = local_ms / args.steps / 1e3
+    achieved_bw = trials_local * term_bytes / kernel_s
+    ncu_path = os.path.join(ROOT, "profiles", "r01_v2_f32_ncu.json")
+    traffic = None
+    issue_frac = None
+    if os.path.exists(ncu_path):
+        try:
+            nj = json.load(open(ncu_path))
+            # DRAM bytes per trial in the profiled launch, scaled to this launch
+            traffic = nj["dram_bytes_per_trial"] * trials_local
+            issue_frac = nj["issue_active_frac"]
+        except (OSError, KeyError, ValueError):
+            pass
     sfu_roof = sm_count * 16 * 1.965e9 / (2 * N_DIM + 1)
 
     line = {
@@ -316,11 +331,17 @@ def main():
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "api": "psa_run_synchronous (C-ABI, host buffers)"},
         "gpu_launches": args.steps * plan.launches_per_run,
-        "roofline": {"bound": "issue", "achieved": achieved_ops / 1e9, "peak": issue_peak / 1e9,
-                     "unit": "Gop/s", "frac": achieved_ops / issue_peak, "traffic": None,
-                     "peak_source": peak_src, "ops_per_trial": ops_per_trial,
+        "roofline": {"bound": "smem", "achieved": achieved_bw / 1e9, "peak": smem_peak / 1e9, "unit": "GB/s",
+                     "frac": achieved_bw / smem_peak, "traffic": traffic,
+                     "kernel": "v2_kernel<float, SepCost<float, Schwefel>, 100> (persistent cooperative)",
+                     "algorithmic_bytes_per_trial": term_bytes, "trials_per_launch": trials_local,
+                     "kernel_ms": kernel_s * 1e3, "peak_source": peak_src,
+                     "traffic_note": "DRAM bytes (ncu, profiles/r01_v2_f32_ncu.json) scaled to this launch; "
+                                     "state is on-chip, so DRAM traffic is ~0",
+                     "issue_active_frac_ncu": issue_frac,
+                     "trials_per_s": trials_local / kernel_s,
                      "sfu_full_eval_roofline_trials_per_s": sfu_roof,
-                     "trials_per_s_vs_sfu_full_eval_roofline": (trials_local / (local_ms / args.steps / 1e3)) / sfu_roof},
+                     "trials_per_s_vs_sfu_full_eval_roofline": (trials_local / kernel_s) / sfu_roof},
         "clocks": clocks,
         "result": {"best_f": res.best_f, "winning_chain": res.winning_chain, "evaluations": res.evaluations},
     }
