@@ -183,6 +183,16 @@ psa_status psa_hybrid_run(const psa_objective* f, const psa_engine_config* cfg,
                           const psa_schedule* truncated, const psa_nm_config* nm,
                           psa_run_result* out);
 
+/* metropolis_sweep, sa_core.cpp:61-79: n_steps Metropolis trials of ONE
+ * caller-held chain on the device.  x (dim doubles) and *energy are the
+ * ChainState (updated in place); (seed, chain, level, *counter) is its
+ * UniformStream (StreamKey + draw counter, advanced by 3*n_steps);
+ * *eval_count is incremented by n_steps (may be NULL).  Precision follows
+ * chain_energy (sa_core.cpp:57-59). */
+psa_status psa_metropolis_sweep(const psa_objective* f, int32_t precision, double* x, double* energy,
+                                uint64_t seed, uint32_t chain, uint32_t level, uint64_t* counter,
+                                double temperature, int32_t n_steps, uint64_t* eval_count);
+
 /* ---- device-resident plans (benchmarks, multi-GPU shards) --------------
  * A plan uploads the problem once, owns the device buffers and launches the
  * persistent engine kernel on a caller-supplied cudaStream_t (as void*), so

@@ -746,6 +746,59 @@ psa_status psa_device_evaluate(const psa_objective* f, int32_t precision, const 
     });
 }
 
+psa_status psa_metropolis_sweep(const psa_objective* f, int32_t precision, double* x, double* energy,
+                                uint64_t seed, uint32_t chain, uint32_t level, uint64_t* counter,
+                                double temperature, int32_t n_steps, uint64_t* eval_count) {
+    return guarded([&] {
+        check_objective(f);
+        if (!x || !energy || !counter) fail(PSA_ERR_INVALID_ARGUMENT, "parsa_b200: null argument");
+        if (n_steps <= 0) return; // the reference loop runs zero times
+        require_device();
+        const int n = f->dim;
+        const int prec = precision == PSA_F32 ? PSA_F32 : PSA_F64;
+        const EngineKernels ks = psa::engine_kernels(prec, f->family, 0);
+        std::vector<double> width(n);
+        for (int k = 0; k < n; ++k) width[k] = f->upper[k] - f->lower[k]; // BoxDomain::width
+        const size_t row_bytes = (prec == PSA_F32 ? 4 : 8) * static_cast<size_t>(n) * 2 + 16;
+        DevBuf<double> d_lo, d_w, d_x, d_e;
+        DevBuf<unsigned long long> d_ctr;
+        DevBuf<unsigned char> d_row;
+        d_lo.alloc(n);
+        d_w.alloc(n);
+        d_x.alloc(n);
+        d_e.alloc(1);
+        d_ctr.alloc(1);
+        d_row.alloc(row_bytes);
+        cuda_check(cudaMemcpy(d_lo.p, f->lower, sizeof(double) * n, cudaMemcpyHostToDevice), "H2D");
+        cuda_check(cudaMemcpy(d_w.p, width.data(), sizeof(double) * n, cudaMemcpyHostToDevice), "H2D");
+        cuda_check(cudaMemcpy(d_x.p, x, sizeof(double) * n, cudaMemcpyHostToDevice), "H2D");
+        cuda_check(cudaMemcpy(d_e.p, energy, sizeof(double), cudaMemcpyHostToDevice), "H2D");
+        const unsigned long long c0 = *counter;
+        cuda_check(cudaMemcpy(d_ctr.p, &c0, sizeof(c0), cudaMemcpyHostToDevice), "H2D");
+        EngineArgs a{};
+        a.n = n;
+        a.family = f->family;
+        a.lower = d_lo.p;
+        a.width = d_w.p;
+        a.keys = psa::make_keys(seed);
+        void* row = d_row.p;
+        double* xp = d_x.p;
+        double* ep = d_e.p;
+        unsigned long long* cp = d_ctr.p;
+        uint32_t ch = chain, lv = level;
+        double T = temperature;
+        int steps = n_steps;
+        void* params[] = {&a, &xp, &row, &ep, &cp, &ch, &lv, &T, &steps};
+        cuda_check(cudaLaunchKernel(ks.sweep, dim3(1), dim3(32), params, 0, 0), "sweep_one");
+        unsigned long long c1 = 0;
+        cuda_check(cudaMemcpy(x, d_x.p, sizeof(double) * n, cudaMemcpyDeviceToHost), "D2H");
+        cuda_check(cudaMemcpy(energy, d_e.p, sizeof(double), cudaMemcpyDeviceToHost), "D2H");
+        cuda_check(cudaMemcpy(&c1, d_ctr.p, sizeof(c1), cudaMemcpyDeviceToHost), "D2H");
+        *counter = c1;
+        if (eval_count) *eval_count += static_cast<uint64_t>(n_steps);
+    });
+}
+
 psa_status psa_device_libm_f32(int32_t fn, const float* x, int32_t count, float* out, int32_t* ok) {
     return guarded([&] {
         require_device();

@@ -594,6 +594,62 @@ __global__ void probe_evaluate(const EngineArgs a, const double* x, int count, d
     out[i] = static_cast<double>(Cost::template energy<0>(row, a.n, a.family));
 }
 
+// metropolis_sweep (sa_core.cpp:61-79) for ONE caller-held chain — the
+// single-chain entry point of the C++ API (parsa::metropolis_sweep); the
+// engines run their own fused sweeps.  One thread walks the stream from an
+// arbitrary 64-bit counter.  The chain's cached values live in a global row;
+// every trial re-folds the whole row, so the energy is chain_energy() of the
+// point bit for bit, and the energy carried between trials is the caller's
+// double (state.energy), exactly as the reference carries it.
+template <class R, class Cost>
+__global__ void sweep_one(const EngineArgs a, double* x, R* row, double* energy,
+                          unsigned long long* counter, uint32_t chain, uint32_t level,
+                          double temperature, int n_steps) {
+    constexpr int A = Cost::A;
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const int n = a.n;
+    Box box;
+    box.lower = a.lower;
+    box.width = a.width;
+    box.lo0 = 0;
+    box.w0 = 0;
+    box.uniform = false;
+    for (int k = 0; k < n; ++k) {
+        R t[A];
+        Cost::cache(static_cast<R>(x[k]), k, n, t);
+#pragma unroll
+        for (int q = 0; q < A; ++q) row[k * A + q] = t[q];
+    }
+    double E = *energy;
+    unsigned long long ctr = *counter;
+    const float inv_t = 1.0f / static_cast<float>(temperature);
+    for (int s = 0; s < n_steps; ++s) {
+        const int d = coordinate_index(bits_to_uniform(draw_bits53(ctr, chain, level, a.keys)), n);
+        const double xv = box.point(d, bits_to_uniform(draw_bits53(ctr + 1, chain, level, a.keys)));
+        const double xold = x[d];
+        R to[A], tn[A];
+        Cost::cache(static_cast<R>(xv), d, n, tn);
+#pragma unroll
+        for (int q = 0; q < A; ++q) {
+            to[q] = row[d * A + q];
+            row[d * A + q] = tn[q];
+        }
+        x[d] = xv;
+        const double trial = static_cast<double>(Cost::template energy<0>(row, n, a.family));
+        const uint64_t m3 = draw_bits53(ctr + 2, chain, level, a.keys);
+        ctr += 3;
+        if (metropolis_decide<R>(trial - E, temperature, inv_t, m3)) {
+            E = trial;
+        } else {
+            x[d] = xold;
+#pragma unroll
+            for (int q = 0; q < A; ++q) row[d * A + q] = to[q];
+        }
+    }
+    *energy = E;
+    *counter = ctr;
+}
+
 // ---------------------------------------------------------------------------
 // Host-side dispatch over (precision, family)
 // ---------------------------------------------------------------------------
@@ -605,6 +661,7 @@ struct KernelSet {
         k.v2 = reinterpret_cast<const void*>(&v2_kernel<R, Cost, NT>);
         k.v1 = reinterpret_cast<const void*>(&v1_kernel<R, Cost, NT>);
         k.eval = reinterpret_cast<const void*>(&probe_evaluate<R, Cost>);
+        k.sweep = reinterpret_cast<const void*>(&sweep_one<R, Cost>);
         k.smem_v2 = [](int n, int B) { return engine_smem_bytes<R, Cost::A>(n, B, false); };
         k.smem_v1 = [](int n, int B) { return engine_smem_bytes<R, Cost::A>(n, B, true); };
         k.smem_eval = [](int n, int B) { return sizeof(R) * size_t(row_stride<R>(n, Cost::A)) * B; };

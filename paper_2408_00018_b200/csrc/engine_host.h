@@ -88,6 +88,7 @@ struct EngineKernels {
     const void* v2;
     const void* v1;
     const void* eval;
+    const void* sweep; // sweep_one: single caller-held chain (parsa::metropolis_sweep)
     size_t (*smem_v2)(int n, int B);
     size_t (*smem_v1)(int n, int B);
     size_t (*smem_eval)(int n, int B);

