@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <sstream>
 #include <string>
@@ -183,7 +184,10 @@ struct psa_plan {
     int block = 128, grid = 0;
     size_t smem = 0;
     EngineArgs args{};
-    DevBuf<double> d_lower, d_width, d_start, d_temps, d_trace, d_bestx, d_xbest, d_winner_f;
+    bool hbm_rows = false;        // chain rows in HBM (large n) instead of shared memory
+    const void* kernel = nullptr; // the engine kernel this plan launches
+    DevBuf<double> d_lower, d_width, d_start, d_temps, d_trace, d_bestx, d_xbest, d_winner_f, d_xrows;
+    DevBuf<unsigned char> d_rows;
     DevBuf<int32_t> d_winner;
     DevBuf<uint32_t> d_masks;
     DevBuf<Cand> d_cand, d_cand_start, d_trace_cand;
@@ -249,11 +253,21 @@ void plan_build(psa_plan* p, const psa_objective* f, const psa_engine_config* cf
     auto smem_of = [&](int B) { return engine == 1 ? p->ks.smem_v1(n, B) : p->ks.smem_v2(n, B); };
     int B = 128;
     while (B > 32 && smem_of(B) > smem_cap) B /= 2;
-    if (smem_of(B) > smem_cap)
-        fail(PSA_ERR_INVALID_ARGUMENT, "parsa_b200: dimension too large for the shared-memory chain state");
+    // chain rows that do not fit in shared memory even at 32 threads per
+    // block go to the HBM structure-of-arrays layout (large n)
+    // (PSA_FORCE_HBM_ROWS=1 selects it at any n: the parity tests compare the
+    // two layouts bit for bit)
+    const char* force = std::getenv("PSA_FORCE_HBM_ROWS");
+    p->hbm_rows = smem_of(B) > smem_cap || (force && force[0] == '1');
+    if (p->hbm_rows) {
+        B = 128;
+        if (p->ks.smem_g(n, B) > smem_cap)
+            fail(PSA_ERR_INVALID_ARGUMENT, "parsa_b200: dimension too large for the block-shared level state");
+    }
     p->block = B;
-    p->smem = smem_of(B);
-    const void* kern = engine == 1 ? p->ks.v1 : p->ks.v2;
+    p->smem = p->hbm_rows ? p->ks.smem_g(n, B) : smem_of(B);
+    const void* kern = engine == 1 ? (p->hbm_rows ? p->ks.v1g : p->ks.v1) : (p->hbm_rows ? p->ks.v2g : p->ks.v2);
+    p->kernel = kern;
     cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(p->smem)),
                "cudaFuncSetAttribute");
@@ -287,7 +301,10 @@ void plan_build(psa_plan* p, const psa_objective* f, const psa_engine_config* cf
         p->d_cand.alloc(p->grid);
         p->d_trace_cand.alloc(static_cast<size_t>(p->levels) * p->grid);
         p->d_xbest.alloc(static_cast<size_t>(p->grid) * B * n);
+        p->d_xrows.alloc(static_cast<size_t>(p->grid) * B * n);
     }
+    const size_t threads = static_cast<size_t>(p->grid) * B;
+    if (p->hbm_rows) p->d_rows.alloc(threads * static_cast<size_t>(n) * p->ks.state_bytes);
 
     EngineArgs& a = p->args;
     a.n = n;
@@ -306,6 +323,9 @@ void plan_build(psa_plan* p, const psa_objective* f, const psa_engine_config* cf
     a.chains_local = static_cast<size_t>(p->chains_local);
     a.chain_begin = p->chain_begin;
     a.chains_total = p->chains_total;
+    a.rows = p->d_rows.p;
+    a.xrows = p->d_xrows.p;
+    a.threads = threads;
     a.masks = p->d_masks.p;
     a.cand = p->d_cand.p;
     a.cand_start = p->d_cand_start.p;
@@ -351,10 +371,10 @@ void plan_launch(psa_plan* p, cudaStream_t s) {
     p->args.epoch = ++p->epoch; // mailbox records of this launch carry the epoch
     void* params[] = {&p->args};
     if (p->engine == 2) {
-        cuda_check(cudaLaunchCooperativeKernel(p->ks.v2, dim3(p->grid), dim3(p->block), params, p->smem, s),
+        cuda_check(cudaLaunchCooperativeKernel(p->kernel, dim3(p->grid), dim3(p->block), params, p->smem, s),
                    "launch v2_kernel");
     } else {
-        cuda_check(cudaLaunchKernel(p->ks.v1, dim3(p->grid), dim3(p->block), params, p->smem, s),
+        cuda_check(cudaLaunchKernel(p->kernel, dim3(p->grid), dim3(p->block), params, p->smem, s),
                    "launch v1_kernel");
         int blocks = p->grid;
         void* fparams[] = {&p->args, &blocks};

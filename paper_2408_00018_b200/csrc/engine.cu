@@ -57,14 +57,13 @@ struct Smem {
 };
 
 template <class R, int A>
-size_t engine_smem_bytes(int n, int B, bool with_x) {
+size_t engine_smem_bytes(int n, int B, bool rows_in_smem) {
     size_t off = 0;
     auto take = [&](size_t bytes) {
         off = (off + 15) & ~size_t(15);
         off += bytes;
     };
-    take(sizeof(R) * size_t(row_stride<R>(n, A)) * B); // per-thread state rows
-    if (with_x) take(sizeof(double) * size_t(n) * B);    // per-thread x (async engine)
+    if (rows_in_smem) take(sizeof(R) * size_t(row_stride<R>(n, A)) * B); // per-thread state rows
     take(sizeof(double) * n);            // x*
     take(sizeof(R) * size_t(n) * A);     // V*
     take(sizeof(double) * n);            // lower
@@ -108,6 +107,22 @@ __device__ void cache_point(const double* xs, R* vs, int n, int family) {
     }
     (void)family;
 }
+
+// The thread's chain-state row: shared memory (G = false) or HBM SoA (G = true)
+template <class R, bool G>
+struct RowSel;
+template <class R>
+struct RowSel<R, false> {
+    using T = R*;
+    static __device__ T make(R* V, int S, const EngineArgs&, size_t) { return V + static_cast<size_t>(threadIdx.x) * S; }
+};
+template <class R>
+struct RowSel<R, true> {
+    using T = StridedRow<R>;
+    static __device__ T make(R*, int, const EngineArgs& a, size_t gtid) {
+        return T{static_cast<R*>(a.rows) + gtid, a.threads};
+    }
+};
 
 // draw_random_start (engines.cpp:43-46): coordinate k uses draw k of (seed, c, 0)
 __device__ __forceinline__ double random_start_coord(const EngineArgs& a, const Box& box,
@@ -237,7 +252,7 @@ __device__ void exchange_level(const EngineArgs& a, double* xs, Cand& w, Cand& w
 // V2 persistent kernel
 // ---------------------------------------------------------------------------
 
-template <class R, class Cost, int NT>
+template <class R, class Cost, int NT, bool G>
 __global__ void __launch_bounds__(PSA_V2_MAX_THREADS, PSA_V2_MIN_BLOCKS) v2_kernel(const EngineArgs a) {
     constexpr int A = Cost::A;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -245,8 +260,8 @@ __global__ void __launch_bounds__(PSA_V2_MAX_THREADS, PSA_V2_MIN_BLOCKS) v2_kern
     const int B = blockDim.x, tid = threadIdx.x;
     const int n = a.n;
     Smem sm{smem_raw};
-    const int S = row_stride<R>(n, A);
-    R* V = sm.take<R>(static_cast<size_t>(S) * B);
+    const int S = G ? n * A : row_stride<R>(n, A);
+    R* V = G ? nullptr : sm.take<R>(static_cast<size_t>(S) * B);
     double* xs = sm.take<double>(n);
     R* vs = sm.take<R>(static_cast<size_t>(n) * A);
     double* lower = sm.take<double>(n);
@@ -271,7 +286,7 @@ __global__ void __launch_bounds__(PSA_V2_MAX_THREADS, PSA_V2_MIN_BLOCKS) v2_kern
     const size_t gtid = static_cast<size_t>(blockIdx.x) * B + tid;
     const size_t W = static_cast<size_t>((a.N + 31) / 32);
     const size_t mask_buf = W * a.chains_local;
-    R* row = V + static_cast<size_t>(tid) * S;
+    const auto row = RowSel<R, G>::make(V, S, a, gtid);
     SweepStats st{0, 0};
 
     for (int l = 0; l < a.levels; ++l) {
@@ -290,7 +305,7 @@ __global__ void __launch_bounds__(PSA_V2_MAX_THREADS, PSA_V2_MIN_BLOCKS) v2_kern
 #pragma unroll
                     for (int q = 0; q < A; ++q) row[k * A + q] = t[q];
                 }
-                e = Cost::template energy<NT>(row, n, a.family);
+                e = row_energy<Cost, NT>(row, n, a.family);
                 ctr = static_cast<uint32_t>(n);
                 st.draws += static_cast<uint64_t>(n);
                 const Cand s{static_cast<double>(e), static_cast<int32_t>(c), 0};
@@ -301,7 +316,7 @@ __global__ void __launch_bounds__(PSA_V2_MAX_THREADS, PSA_V2_MIN_BLOCKS) v2_kern
             }
             if (l == 0) st.evals += 1; // the start evaluation (engines.cpp:157)
             e = sweep<R, Cost, NT>(row, n, a.family, e, temperature, c, static_cast<uint32_t>(l), ctr,
-                               a.N, box, a.keys, masks + cl, a.chains_local, nullptr, st);
+                                   a.N, box, a.keys, masks + cl, a.chains_local, nullptr, 0, st);
             const Cand mine{static_cast<double>(e), static_cast<int32_t>(c), 0};
             if (better(mine, best)) best = mine;
         }
@@ -389,16 +404,15 @@ __global__ void __launch_bounds__(PSA_V2_MAX_THREADS, PSA_V2_MIN_BLOCKS) v2_kern
 // cand[gtid] with its point in xbest[gtid].  v1_finalize reduces both.
 // ---------------------------------------------------------------------------
 
-template <class R, class Cost, int NT>
+template <class R, class Cost, int NT, bool G>
 __global__ void __launch_bounds__(256) v1_kernel(const EngineArgs a) {
     constexpr int A = Cost::A;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int B = blockDim.x, tid = threadIdx.x;
     const int n = a.n;
     Smem sm{smem_raw};
-    const int S = row_stride<R>(n, A);
-    R* V = sm.take<R>(static_cast<size_t>(S) * B);
-    double* X = sm.take<double>(static_cast<size_t>(n) * B);
+    const int S = G ? n * A : row_stride<R>(n, A);
+    R* V = G ? nullptr : sm.take<R>(static_cast<size_t>(S) * B);
     double* xs = sm.take<double>(n);
     R* vs = sm.take<R>(static_cast<size_t>(n) * A);
     double* lower = sm.take<double>(n);
@@ -418,8 +432,12 @@ __global__ void __launch_bounds__(256) v1_kernel(const EngineArgs a) {
     const size_t total_threads = static_cast<size_t>(gridDim.x) * B;
     const size_t gtid = static_cast<size_t>(blockIdx.x) * B + tid;
     const size_t rounds = (a.chains_local + total_threads - 1) / total_threads;
-    R* row = V + static_cast<size_t>(tid) * S;
-    double* xrow = X + static_cast<size_t>(tid) * n;
+    const auto row = RowSel<R, G>::make(V, S, a, gtid);
+    // the chain's double-precision point: written once per accepted move, so
+    // it lives in HBM (SoA, stride = threads) and leaves shared memory to the
+    // cached terms the fold reads on every trial
+    double* xrow = a.xrows + gtid;
+    const size_t xst = a.threads;
     SweepStats st{0, 0};
     Cand mybest = empty_cand();
 
@@ -433,17 +451,17 @@ __global__ void __launch_bounds__(256) v1_kernel(const EngineArgs a) {
             if (a.random_start) {
                 for (int k = 0; k < n; ++k) {
                     const double xk = random_start_coord(a, box, c, k);
-                    xrow[k] = xk;
+                    xrow[k * xst] = xk;
                     R t[A];
                     Cost::cache(static_cast<R>(xk), k, n, t);
 #pragma unroll
                     for (int q = 0; q < A; ++q) row[k * A + q] = t[q];
                 }
-                e = Cost::template energy<NT>(row, n, a.family);
+                e = row_energy<Cost, NT>(row, n, a.family);
                 ctr = static_cast<uint32_t>(n);
                 st.draws += static_cast<uint64_t>(n);
             } else {
-                for (int k = 0; k < n; ++k) xrow[k] = xs[k];
+                for (int k = 0; k < n; ++k) xrow[k * xst] = xs[k];
                 for (int k = 0; k < n * A; ++k) row[k] = vs[k];
                 e = static_cast<R>(sh->estar);
             }
@@ -453,7 +471,7 @@ __global__ void __launch_bounds__(256) v1_kernel(const EngineArgs a) {
         for (int l = 0; l < a.levels; ++l) {
             if (active) {
                 e = sweep<R, Cost, NT>(row, n, a.family, e, a.temps[l], c, 0, ctr, a.N, box, a.keys,
-                                   nullptr, 0, xrow, st);
+                                       nullptr, 0, xrow, xst, st);
                 ctr += 3u * static_cast<uint32_t>(a.N);
                 // std::min(chain_best, energy) (engines.cpp:94)
                 if (static_cast<double>(e) < chain_best) chain_best = static_cast<double>(e);
@@ -474,7 +492,7 @@ __global__ void __launch_bounds__(256) v1_kernel(const EngineArgs a) {
             if (better(mine, mybest)) {
                 mybest = mine;
                 for (int k = 0; k < n; ++k)
-                    a.xbest[gtid * static_cast<size_t>(n) + k] = xrow[k];
+                    a.xbest[gtid * static_cast<size_t>(n) + k] = xrow[k * xst];
             }
         }
     }
@@ -658,11 +676,15 @@ template <class R, class Cost, int NT = 0>
 struct KernelSet {
     static EngineKernels get() {
         EngineKernels k;
-        k.v2 = reinterpret_cast<const void*>(&v2_kernel<R, Cost, NT>);
-        k.v1 = reinterpret_cast<const void*>(&v1_kernel<R, Cost, NT>);
+        k.v2 = reinterpret_cast<const void*>(&v2_kernel<R, Cost, NT, false>);
+        k.v1 = reinterpret_cast<const void*>(&v1_kernel<R, Cost, NT, false>);
+        k.v2g = reinterpret_cast<const void*>(&v2_kernel<R, Cost, 0, true>);
+        k.v1g = reinterpret_cast<const void*>(&v1_kernel<R, Cost, 0, true>);
+        k.smem_g = [](int n, int B) { return engine_smem_bytes<R, Cost::A>(n, B, false); };
+        k.state_bytes = sizeof(R) * Cost::A;
         k.eval = reinterpret_cast<const void*>(&probe_evaluate<R, Cost>);
         k.sweep = reinterpret_cast<const void*>(&sweep_one<R, Cost>);
-        k.smem_v2 = [](int n, int B) { return engine_smem_bytes<R, Cost::A>(n, B, false); };
+        k.smem_v2 = [](int n, int B) { return engine_smem_bytes<R, Cost::A>(n, B, true); };
         k.smem_v1 = [](int n, int B) { return engine_smem_bytes<R, Cost::A>(n, B, true); };
         k.smem_eval = [](int n, int B) { return sizeof(R) * size_t(row_stride<R>(n, Cost::A)) * B; };
         return k;

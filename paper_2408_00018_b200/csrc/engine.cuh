@@ -50,6 +50,26 @@ struct Vec16<double> {
     PSA_DEV static double get(const double2& v, int i) { return i == 0 ? v.x : v.y; }
 };
 
+// Large-n layout: when a thread's row does not fit in shared memory the rows
+// live in HBM, structure-of-arrays: value i of thread g at base[i*T + g]
+// (T = threads in the grid), so a warp's accesses to the same i are one
+// coalesced 128-byte (f32) / 256-byte (f64) transaction.
+template <class R>
+struct StridedRow {
+    R* p;
+    size_t s;
+    PSA_DEV R& operator[](int i) const { return p[static_cast<size_t>(i) * s]; }
+};
+
+template <class T>
+struct IsStrided {
+    static constexpr bool value = false;
+};
+template <class R>
+struct IsStrided<StridedRow<R>> {
+    static constexpr bool value = true;
+};
+
 // ---------------------------------------------------------------------------
 // Cost interface
 // ---------------------------------------------------------------------------
@@ -133,11 +153,24 @@ struct SepCost {
         }
         return Fam::finish(acc, n);
     }
+    // any row type with operator[] (the HBM layout): scalar loads, same order
+    template <class Row>
+    PSA_DEV static R energy_any(const Row& row, int n, int) {
+        R acc[A];
+#pragma unroll
+        for (int a = 0; a < A; ++a) acc[a] = Fam::init(a, n);
+#pragma unroll 4
+        for (int k = 0; k < n; ++k) {
+#pragma unroll
+            for (int a = 0; a < A; ++a) acc[a] = fold<R>(Fam::op(a), acc[a], row[k * A + a]);
+        }
+        return Fam::finish(acc, n);
+    }
 };
 
-template <class R>
+template <class R, class Row = const R*>
 struct RowX {
-    const R* row;
+    Row row;
     PSA_DEV R operator()(int k) const { return row[k]; }
 };
 
@@ -151,7 +184,11 @@ struct FullCost {
     }
     template <int NT = 0>
     PSA_DEV static R energy(const R* row, int n, int family) {
-        const RowX<R> x{row};
+        return energy_any(row, n, family);
+    }
+    template <class Row>
+    PSA_DEV static R energy_any(const Row& row, int n, int family) {
+        const RowX<R, Row> x{row};
         switch (family) {
         case PSA_FN_BRANIN: return Branin<R>::eval(x, n);
         case PSA_FN_DEKKERS_AARTS: return DekkersAarts<R>::eval(x, n);
@@ -170,6 +207,13 @@ struct FullCost {
         }
     }
 };
+
+// energy of a chain row of either layout
+template <class Cost, int NT, class Row>
+PSA_DEV auto row_energy(const Row& row, int n, int family) {
+    if constexpr (IsStrided<Row>::value) return Cost::energy_any(row, n, family);
+    else return Cost::template energy<NT>(row, n, family);
+}
 
 // ---------------------------------------------------------------------------
 // Metropolis rule — sa_core.cpp:46-55 (the draw is consumed by the caller)
@@ -240,19 +284,20 @@ struct SweepStats {
     uint64_t draws;
 };
 
-// row: this thread's 16-byte aligned state row.  Returns the end energy;
-// accept bits go to mask[w*mask_stride], w = j/32.  If x != nullptr
+// row: this thread's 16-byte aligned shared-memory state row (Row = R*), or
+// its HBM structure-of-arrays row (Row = StridedRow<R>).  Returns the end
+// energy; accept bits go to mask[w*mask_stride], w = j/32.  If x != nullptr
 // (asynchronous engine), accepted coordinates are also written to the
-// double-precision point x[k] of this chain.
+// double-precision point of this chain, x[k * x_stride].
 //
 // The three draws of trial j+1 do not depend on trial j's outcome (the
 // streams are counter-based), so they are issued before the fold of trial j
 // and overlap its dependent FADD chain; the acceptance draw is therefore
 // computed even for downhill moves (it is consumed either way, rng.hpp).
-template <class R, class Cost, int NT = 0>
-PSA_DEV R sweep(R* row, int n_rt, int family, R E, double temperature, uint32_t chain,
+template <class R, class Cost, int NT = 0, class Row = R*>
+PSA_DEV R sweep(Row row, int n_rt, int family, R E, double temperature, uint32_t chain,
                 uint32_t level, uint32_t ctr, int N, const Box& box, const PhiloxKeys& keys,
-                uint32_t* mask, size_t mask_stride, double* x, SweepStats& st) {
+                uint32_t* mask, size_t mask_stride, double* x, size_t x_stride, SweepStats& st) {
     constexpr int A = Cost::A;
     const int n = NT > 0 ? NT : n_rt;
     const float inv_t = 1.0f / static_cast<float>(temperature);
@@ -273,11 +318,10 @@ PSA_DEV R sweep(R* row, int n_rt, int family, R E, double temperature, uint32_t 
     }
     for (int j = 0; j < N; ++j) {
         R to[A];
-        R* slot = row + d * A;
 #pragma unroll
         for (int a = 0; a < A; ++a) {
-            to[a] = slot[a];
-            slot[a] = tn[a];
+            to[a] = row[d * A + a];
+            row[d * A + a] = tn[a];
         }
         // independent of this trial's outcome: its acceptance draw and the
         // next proposal (the streams are counter-based)
@@ -299,7 +343,7 @@ PSA_DEV R sweep(R* row, int n_rt, int family, R E, double temperature, uint32_t 
             else asm volatile("" ::"d"(tnn[a]));
         }
 #endif
-        const R trial = Cost::template energy<NT>(row, n, family);
+        const R trial = row_energy<Cost, NT>(row, n, family);
         if (!ok) Cost::cache(static_cast<R>(xn), dn, n, tnn); // general path, practically never
 
         const double delta_e = static_cast<double>(trial) - static_cast<double>(E);
@@ -309,10 +353,10 @@ PSA_DEV R sweep(R* row, int n_rt, int family, R E, double temperature, uint32_t 
         if (acc) {
             E = trial;
             word |= 1u << (j & 31);
-            if (x) x[d] = xnew;
+            if (x) x[static_cast<size_t>(d) * x_stride] = xnew;
         } else {
 #pragma unroll
-            for (int a = 0; a < A; ++a) slot[a] = to[a];
+            for (int a = 0; a < A; ++a) row[d * A + a] = to[a];
         }
         if ((j & 31) == 31 || j == N - 1) {
             if (mask) mask[static_cast<size_t>(j >> 5) * mask_stride] = word;

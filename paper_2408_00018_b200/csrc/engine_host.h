@@ -42,6 +42,9 @@ struct EngineArgs {
     size_t chains_local;   // chains in this shard
     uint32_t chain_begin;  // global index of the shard's first chain
     uint32_t chains_total;
+    void* rows;            // HBM layout only: [n*A][threads] chain state (R elements)
+    double* xrows;         // V1: [n][threads] double-precision point of each thread's chain
+    size_t threads;        // grid * block (the SoA stride of rows/xrows)
     uint32_t* masks;       // V2: [2][ceil(N/32)][chains_local] accept bits
     Cand* cand;            // V2: [2][grid]; V1: [grid]
     Cand* cand_start;      // V2 random start: [grid]
@@ -87,6 +90,10 @@ struct NMArgsHost {
 struct EngineKernels {
     const void* v2;
     const void* v1;
+    const void* v2g; // HBM chain-state layout (large n)
+    const void* v1g;
+    size_t (*smem_g)(int n, int B);
+    size_t state_bytes; // sizeof(R) * A: bytes per coordinate of a chain row
     const void* eval;
     const void* sweep; // sweep_one: single caller-held chain (parsa::metropolis_sweep)
     size_t (*smem_v2)(int n, int B);

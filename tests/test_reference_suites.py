@@ -20,6 +20,7 @@ reference harness's output (wall-time fields masked; make_harness_golden.py).
 """
 from __future__ import annotations
 
+import json
 import os
 import re
 import subprocess
@@ -127,7 +128,12 @@ def test_cli_reports_match_reference_bytes(spec):
     src = os.path.join(GOLDEN, spec)
     with tempfile.TemporaryDirectory() as d:
         cfg = os.path.join(src, "config.json")
-        p = subprocess.run([CLI, "run", "--config", cfg], cwd=d, capture_output=True, text=True, timeout=600)
+        with open(cfg) as fh:
+            engine = json.load(fh)["engine"]
+        # the CLI's --engine defaults to v2 and overrides the config file's
+        # engine (parsa_main.cpp:23,57), so the engine is passed explicitly
+        p = subprocess.run([CLI, "run", "--config", cfg, "--engine", engine], cwd=d, capture_output=True,
+                           text=True, timeout=600)
         assert p.returncode == 0, p.stderr
         want = sorted(f for f in os.listdir(src) if f != "config.json")
         got = sorted(os.listdir(d))
