@@ -185,6 +185,8 @@ struct psa_plan {
     size_t smem = 0;
     EngineArgs args{};
     bool hbm_rows = false;        // chain rows in HBM (large n) instead of shared memory
+    bool pair = false;            // two chains per thread (v2_pair_kernel)
+    size_t mask_stride = 0;
     const void* kernel = nullptr; // the engine kernel this plan launches
     DevBuf<double> d_lower, d_width, d_start, d_temps, d_trace, d_bestx, d_xbest, d_winner_f, d_xrows;
     DevBuf<unsigned char> d_rows;
@@ -267,6 +269,23 @@ void plan_build(psa_plan* p, const psa_objective* f, const psa_engine_config* cf
     p->block = B;
     p->smem = p->hbm_rows ? p->ks.smem_g(n, B) : smem_of(B);
     const void* kern = engine == 1 ? (p->hbm_rows ? p->ks.v1g : p->ks.v1) : (p->hbm_rows ? p->ks.v2g : p->ks.v2);
+    // binary32 separable families: two chains per thread (FADD2 fold) when
+    // the pair rows fit (PSA_NO_PAIR=1 keeps one chain per thread)
+    // V2 kernel choice (PSA_V2_MODE = single | pair overrides, for A/B
+    // measurements; both are bit-identical)
+    const char* mode_env = std::getenv("PSA_V2_MODE");
+    const std::string mode = mode_env ? mode_env : "";
+    const char* no_pair = std::getenv("PSA_NO_PAIR");
+    if (engine == 2 && !p->hbm_rows && p->ks.v2p && mode != "single" && !(no_pair && no_pair[0] == '1')) {
+        int Bp = 128;
+        while (Bp > 32 && p->ks.smem_v2p(n, Bp) > smem_cap) Bp /= 2;
+        if (p->ks.smem_v2p(n, Bp) <= smem_cap) {
+            p->pair = true;
+            p->block = B = Bp;
+            p->smem = p->ks.smem_v2p(n, Bp);
+            kern = p->ks.v2p;
+        }
+    }
     p->kernel = kern;
     cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(p->smem)),
@@ -274,7 +293,8 @@ void plan_build(psa_plan* p, const psa_objective* f, const psa_engine_config* cf
     int per_sm = 0;
     cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, B, p->smem), "occupancy");
     if (per_sm < 1) fail(PSA_ERR_CUDA, "parsa_b200: engine kernel cannot be resident");
-    const long long need = (static_cast<long long>(p->chains_local) + B - 1) / B;
+    const long long units = p->pair ? (static_cast<long long>(p->chains_local) + 1) / 2 : p->chains_local;
+    const long long need = (units + B - 1) / B;
     p->grid = static_cast<int>(std::min<long long>(need, static_cast<long long>(per_sm) * prop.multiProcessorCount));
     if (p->max_blocks > 0) p->grid = std::min(p->grid, p->max_blocks);
 
@@ -291,8 +311,9 @@ void plan_build(psa_plan* p, const psa_objective* f, const psa_engine_config* cf
     cuda_check(cudaMemcpy(p->d_start.p, start.data(), sizeof(double) * n, cudaMemcpyHostToDevice), "H2D");
     cuda_check(cudaMemcpy(p->d_temps.p, p->temps.data(), sizeof(double) * p->levels, cudaMemcpyHostToDevice), "H2D");
     const size_t W = (p->N + 31) / 32;
+    p->mask_stride = (static_cast<size_t>(p->chains_local) + 1) & ~size_t(1);
     if (engine == 2) {
-        p->d_masks.alloc(2 * W * static_cast<size_t>(p->chains_local));
+        p->d_masks.alloc(2 * W * static_cast<size_t>(p->mask_stride));
         p->d_cand.alloc(2 * static_cast<size_t>(p->grid));
         p->d_cand_start.alloc(p->grid);
         p->d_winner.alloc(p->levels);
@@ -327,6 +348,7 @@ void plan_build(psa_plan* p, const psa_objective* f, const psa_engine_config* cf
     a.xrows = p->d_xrows.p;
     a.threads = threads;
     a.masks = p->d_masks.p;
+    a.mask_stride = p->mask_stride;
     a.cand = p->d_cand.p;
     a.cand_start = p->d_cand_start.p;
     a.trace_cand = p->d_trace_cand.p;

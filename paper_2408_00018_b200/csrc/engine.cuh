@@ -103,10 +103,18 @@ struct SepCost {
     // straight-line block (no loop), so the scheduler can interleave the
     // next trial's independent Philox work into the FADD dependency chain.
     template <int NT = 0>
-    PSA_DEV static R energy(const R* row, int n_rt, int) {
-        using V = Vec16<R>;
+    PSA_DEV static R energy(const R* row, int n_rt, int family) {
         const int n = NT > 0 ? NT : n_rt;
         R acc[A];
+        fold_acc<NT>(row, n, acc);
+        (void)family;
+        return Fam::finish(acc, n);
+    }
+    // the accumulators of the fold, before finish()
+    template <int NT = 0>
+    PSA_DEV static void fold_acc(const R* row, int n_rt, R* acc) {
+        using V = Vec16<R>;
+        const int n = NT > 0 ? NT : n_rt;
 #pragma unroll
         for (int a = 0; a < A; ++a) acc[a] = Fam::init(a, n);
         const int m = n * A;
@@ -151,7 +159,6 @@ struct SepCost {
             }
             for (int e = mv * V::W; e < m; ++e) acc[e % A] = fold<R>(Fam::op(e % A), acc[e % A], row[e]);
         }
-        return Fam::finish(acc, n);
     }
     // any row type with operator[] (the HBM layout): scalar loads, same order
     template <class Row>
@@ -238,26 +245,35 @@ struct Accept<float> {
     }
 };
 
-// The Metropolis decision with a fast, provably safe pre-test.  With
-// ya = -float(dE) * RN(1/float(T)) (relative error <= 3 ulp of float) and
-// e = __expf(ya) (MUFU.EX2-based), the exact exp(-dE/T) lies within a
-// factor (1 +- 2e-5) of e for every |ya| <= 40; a uniform more than 2^-12
-// (relative) below e is accepted and one above is rejected without the
-// exact test.  For ya < -40 the exact value is below 2^-53, the smallest
-// non-zero uniform, so only u == 0 (m == 0) accepts.  Everything else
-// (the ambiguous band, NaNs) takes the exact glibc-restated path, so the
-// decision is bit-identical to the reference for every input.
+// 2^x, MUFU.EX2 (relative error ~2^-22; subnormal results flush to 0)
+PSA_DEV float ex2_approx(float x) {
+    float r;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
+// The Metropolis decision (sa_core.cpp:46-55) with a branch-free pre-test;
+// returns 1 accept, 0 reject, -1 undecided.
+//  * d = trial - E in R has the sign of the reference's double difference
+//    (subtracting two floats never flips the sign, is zero only for equal
+//    values, and is NaN exactly when the double one is; for R = double it
+//    is the reference's own difference), so d <= 0 is the downhill test.
+//  * e = 2^(-d * log2(e)/T) approximates exp(-dE/T) within a relative
+//    3e-5 wherever it is a normal float (|ln| <= 87.3: rounding of d, of the
+//    per-level factor k2 and of ex2.approx); the uniform (as the reference's
+//    float(u) = RN24(m)*2^-53, or u itself in f64 mode) is compared with e
+//    widened by 2^-12 either way.  Outside that band the answer is certain.
+//    When e flushes to zero, any m >= 1 rejects (the true value is below
+//    2^-125 < 2^-53); m == 0, NaNs and the band itself report undecided and
+//    the caller runs the exact glibc-restated test.
 template <class R>
-PSA_DEV bool metropolis_decide(double delta_e, double temperature, float inv_t, uint64_t m) {
-    if (delta_e <= 0) return true; // sa_core.cpp:50
-    const float ya = -static_cast<float>(delta_e) * inv_t;
-    const float uf = bits_to_uniform_f32(m);
-    const bool tiny = ya < -40.0f;
-    const float e = __expf(ya);
-    const bool sure_acc = tiny ? (m == 0) : (uf < e * (1.0f - 0x1p-12f));
-    const bool sure_rej = tiny ? (m != 0) : (uf > e * (1.0f + 0x1p-12f));
-    if (sure_acc | sure_rej) return sure_acc;
-    return Accept<R>::exact(delta_e, temperature, m);
+PSA_DEV int metropolis_fast(R trial, R E, float k2, uint64_t m) {
+    const R d = trial - E;
+    const float e = ex2_approx(-static_cast<float>(d) * k2);
+    const float fm = __ull2float_rn(m);
+    const bool acc = (d <= R(0)) | (fm < e * 0x1.ffep+52f);  // 2^53 (1 - 2^-12)
+    const bool rej = fm > e * 0x1.001p+53f;                 // 2^53 (1 + 2^-12)
+    return acc ? 1 : (rej ? 0 : -1);
 }
 
 // ---------------------------------------------------------------------------
@@ -300,7 +316,7 @@ PSA_DEV R sweep(Row row, int n_rt, int family, R E, double temperature, uint32_t
                 uint32_t* mask, size_t mask_stride, double* x, size_t x_stride, SweepStats& st) {
     constexpr int A = Cost::A;
     const int n = NT > 0 ? NT : n_rt;
-    const float inv_t = 1.0f / static_cast<float>(temperature);
+    const float k2 = static_cast<float>(1.4426950408889634 / temperature); // log2(e) / T
     const PhiloxChain pc = philox_chain(chain, level, keys);
     const double idx_scale = static_cast<double>(n) * 0x1.0p-53; // u*n == m*(n*2^-53) exactly
     uint32_t word = 0;
@@ -344,11 +360,15 @@ PSA_DEV R sweep(Row row, int n_rt, int family, R E, double temperature, uint32_t
         }
 #endif
         const R trial = row_energy<Cost, NT>(row, n, family);
-        if (!ok) Cost::cache(static_cast<R>(xn), dn, n, tnn); // general path, practically never
+        // rare paths behind warp-uniform branches
+        if (__any_sync(__activemask(), !ok))
+            if (!ok) Cost::cache(static_cast<R>(xn), dn, n, tnn); // general path, practically never
 
-        const double delta_e = static_cast<double>(trial) - static_cast<double>(E);
         // sa_core.cpp:46-55 (the acceptance draw is consumed either way)
-        const bool acc = metropolis_decide<R>(delta_e, temperature, inv_t, m3);
+        int r = metropolis_fast<R>(trial, E, k2, m3);
+        if (__any_sync(__activemask(), r < 0))
+            if (r < 0) r = Accept<R>::exact(static_cast<double>(trial) - static_cast<double>(E), temperature, m3);
+        const bool acc = r != 0;
         ctr += 3;
         if (acc) {
             E = trial;
@@ -370,6 +390,185 @@ PSA_DEV R sweep(Row row, int n_rt, int family, R E, double temperature, uint32_t
     st.evals += static_cast<uint64_t>(N);
     st.draws += 3ull * static_cast<uint64_t>(N);
     return E;
+}
+
+// ---------------------------------------------------------------------------
+// Chain pairs: two chains per thread, folded with packed FP32x2 adds
+//
+// sm_100 issues FADD2/FMUL2 (PTX add/sub/mul.rn.f32x2): two IEEE binary32
+// operations, each rounded exactly like FADD/FMUL, in one instruction.  The
+// term fold is a serial chain per chain, so it cannot be split; but two
+// independent chains (A, B) folded side by side halve the instructions of
+// the fold, which is a third of the trial's issue budget.  Pair rows
+// interleave the chains: element e = k*A + a holds (t_e of A, t_e of B) as
+// one 8-byte word, so a 16-byte LDS feeds two FADD2.
+// ---------------------------------------------------------------------------
+
+struct F2 {
+    unsigned long long v;
+};
+
+PSA_DEV F2 f2_make(float lo, float hi) {
+    F2 r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r.v) : "f"(lo), "f"(hi));
+    return r;
+}
+PSA_DEV void f2_split(F2 x, float& lo, float& hi) { asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(x.v)); }
+
+// the fold step of objectives.cuh (kAdd / kSub / kMul), on both lanes
+PSA_DEV F2 f2_fold(int op, F2 acc, F2 t) {
+    F2 r;
+    if (op == kAdd) asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(acc.v), "l"(t.v));
+    else if (op == kSub) asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(acc.v), "l"(t.v));
+    else asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(acc.v), "l"(t.v));
+    return r;
+}
+
+// energies of both chains of a pair row (n*A interleaved elements)
+template <class Fam, int NT>
+PSA_DEV void pair_energy(const float* row, int n_rt, float& eA, float& eB) {
+    constexpr int A = Fam::kArrays;
+    const int n = NT > 0 ? NT : n_rt;
+    const unsigned long long* u = reinterpret_cast<const unsigned long long*>(row);
+    F2 acc[A];
+#pragma unroll
+    for (int a = 0; a < A; ++a) {
+        const float i0 = Fam::init(a, n);
+        acc[a] = f2_make(i0, i0);
+    }
+    if constexpr (NT > 0) {
+        constexpr int M = NT * A;     // elements
+        constexpr int NV = M / 2;     // 16-byte vectors
+        const ulonglong2* p = reinterpret_cast<const ulonglong2*>(u);
+#ifndef PSA_PAIR_PREFETCH
+#define PSA_PAIR_PREFETCH 4
+#endif
+        constexpr int PF = PSA_PAIR_PREFETCH < NV ? PSA_PAIR_PREFETCH : NV;
+        ulonglong2 buf[PF > 0 ? PF : 1];
+#pragma unroll
+        for (int q = 0; q < PF; ++q) buf[q] = p[q];
+#pragma unroll
+        for (int q = 0; q < NV; ++q) {
+            const ulonglong2 v = buf[q % PF];
+            if (q + PF < NV) buf[q % PF] = p[q + PF];
+            acc[(2 * q) % A] = f2_fold(Fam::op((2 * q) % A), acc[(2 * q) % A], F2{v.x});
+            acc[(2 * q + 1) % A] = f2_fold(Fam::op((2 * q + 1) % A), acc[(2 * q + 1) % A], F2{v.y});
+        }
+        if constexpr (M % 2) acc[(M - 1) % A] = f2_fold(Fam::op((M - 1) % A), acc[(M - 1) % A], F2{u[M - 1]});
+    } else {
+        const int M = n * A;
+#pragma unroll 4
+        for (int e = 0; e < M; ++e) acc[e % A] = f2_fold(Fam::op(e % A), acc[e % A], F2{u[e]});
+    }
+    float ra[A], rb[A];
+#pragma unroll
+    for (int a = 0; a < A; ++a) f2_split(acc[a], ra[a], rb[a]);
+    eA = Fam::finish(ra, n);
+    eB = Fam::finish(rb, n);
+}
+
+
+// One level of N trials for the chain pair (cA, cB) of a pair row: the
+// sweep() of sa_core.cpp:61-79 for two chains at once.  Each chain's draws,
+// proposals, energies and decisions are exactly those of sweep(); only the
+// fold is shared (FADD2).  Accept bits go to maskA/maskB[w * mask_stride].
+template <template <class> class F, int NT>
+PSA_DEV void sweep_pair(float* row, int n_rt, float& EA, float& EB, double temperature, uint32_t cA,
+                        uint32_t cB, uint32_t level, uint32_t ctr, int N, const Box& box, const PhiloxKeys& keys,
+                        uint32_t* maskA, uint32_t* maskB, size_t mask_stride) {
+    using Fam = F<float>;
+    using Cost = SepCost<float, F>;
+    constexpr int A = Fam::kArrays;
+    const int n = NT > 0 ? NT : n_rt;
+    const float k2 = static_cast<float>(1.4426950408889634 / temperature); // log2(e) / T
+    const PhiloxChain pa = philox_chain(cA, level, keys);
+    const PhiloxChain pb = philox_chain(cB, level, keys);
+    const double idx_scale = static_cast<double>(n) * 0x1.0p-53;
+    uint32_t wordA = 0, wordB = 0;
+    int dA, dB;
+    double xA, xB;
+    float tA[A], tB[A];
+    {
+        const uint64_t a1 = draw_bits53_fast(ctr, pa, keys), a2 = draw_bits53_fast(ctr + 1, pa, keys);
+        const uint64_t b1 = draw_bits53_fast(ctr, pb, keys), b2 = draw_bits53_fast(ctr + 1, pb, keys);
+        dA = min(static_cast<int>(static_cast<double>(a1) * idx_scale), n - 1);
+        dB = min(static_cast<int>(static_cast<double>(b1) * idx_scale), n - 1);
+        xA = box.point(dA, bits_to_uniform(a2));
+        xB = box.point(dB, bits_to_uniform(b2));
+        Cost::cache(static_cast<float>(xA), dA, n, tA);
+        Cost::cache(static_cast<float>(xB), dB, n, tB);
+    }
+    for (int j = 0; j < N; ++j) {
+        float oA[A], oB[A];
+#pragma unroll
+        for (int a = 0; a < A; ++a) {
+            float* sa = row + 2 * (dA * A + a);
+            float* sb = row + 2 * (dB * A + a) + 1;
+            oA[a] = *sa;
+            *sa = tA[a];
+            oB[a] = *sb;
+            *sb = tB[a];
+        }
+        // independent of this trial's outcome: its acceptance draws and the
+        // next proposals (counter-based streams)
+        const uint64_t mA = draw_bits53_fast(ctr + 2, pa, keys);
+        const uint64_t mB = draw_bits53_fast(ctr + 2, pb, keys);
+        const uint64_t a1 = draw_bits53_fast(ctr + 3, pa, keys), a2 = draw_bits53_fast(ctr + 4, pa, keys);
+        const uint64_t b1 = draw_bits53_fast(ctr + 3, pb, keys), b2 = draw_bits53_fast(ctr + 4, pb, keys);
+        const int nA = min(static_cast<int>(static_cast<double>(a1) * idx_scale), n - 1);
+        const int nB = min(static_cast<int>(static_cast<double>(b1) * idx_scale), n - 1);
+        const double yA = box.point(nA, bits_to_uniform(a2));
+        const double yB = box.point(nB, bits_to_uniform(b2));
+        float uA[A], uB[A];
+        bool okA, okB;
+        Cost::cache_common(static_cast<float>(yA), nA, n, uA, okA);
+        Cost::cache_common(static_cast<float>(yB), nB, n, uB, okB);
+#ifndef PSA_PAIR_NO_PIN
+        asm volatile("" ::"l"(mA), "l"(mB), "r"(nA), "r"(nB));
+#pragma unroll
+        for (int a = 0; a < A; ++a) asm volatile("" ::"f"(uA[a]), "f"(uB[a]));
+#endif
+
+        float trA, trB;
+        pair_energy<Fam, NT>(row, n, trA, trB);
+        // rare paths behind warp-uniform branches (no reconvergence barrier
+        // on the common path)
+        if (__any_sync(__activemask(), !(okA & okB))) {
+            if (!okA) Cost::cache(static_cast<float>(yA), nA, n, uA);
+            if (!okB) Cost::cache(static_cast<float>(yB), nB, n, uB);
+        }
+        int rA = metropolis_fast<float>(trA, EA, k2, mA);
+        int rB = metropolis_fast<float>(trB, EB, k2, mB);
+        if (__any_sync(__activemask(), (rA < 0) | (rB < 0))) {
+            if (rA < 0) rA = Accept<float>::exact(static_cast<double>(trA) - static_cast<double>(EA), temperature, mA);
+            if (rB < 0) rB = Accept<float>::exact(static_cast<double>(trB) - static_cast<double>(EB), temperature, mB);
+        }
+        ctr += 3;
+        EA = rA ? trA : EA;
+        EB = rB ? trB : EB;
+        wordA |= static_cast<uint32_t>(rA) << (j & 31);
+        wordB |= static_cast<uint32_t>(rB) << (j & 31);
+#pragma unroll
+        for (int a = 0; a < A; ++a) {
+            if (!rA) row[2 * (dA * A + a)] = oA[a];
+            if (!rB) row[2 * (dB * A + a) + 1] = oB[a];
+        }
+        if ((j & 31) == 31 || j == N - 1) {
+            maskA[static_cast<size_t>(j >> 5) * mask_stride] = wordA;
+            maskB[static_cast<size_t>(j >> 5) * mask_stride] = wordB;
+            wordA = 0;
+            wordB = 0;
+        }
+        dA = nA;
+        dB = nB;
+#pragma unroll
+        for (int a = 0; a < A; ++a) {
+            tA[a] = uA[a];
+            tB[a] = uB[a];
+        }
+    }
+    (void)xA;
+    (void)xB;
 }
 
 // ---------------------------------------------------------------------------

@@ -45,7 +45,8 @@ struct EngineArgs {
     void* rows;            // HBM layout only: [n*A][threads] chain state (R elements)
     double* xrows;         // V1: [n][threads] double-precision point of each thread's chain
     size_t threads;        // grid * block (the SoA stride of rows/xrows)
-    uint32_t* masks;       // V2: [2][ceil(N/32)][chains_local] accept bits
+    uint32_t* masks;       // V2: [2][ceil(N/32)][mask_stride] accept bits
+    size_t mask_stride;    // chains_local, rounded up to even (chain pairs)
     Cand* cand;            // V2: [2][grid]; V1: [grid]
     Cand* cand_start;      // V2 random start: [grid]
     Cand* trace_cand;      // V1: [levels][grid]
@@ -90,6 +91,8 @@ struct NMArgsHost {
 struct EngineKernels {
     const void* v2;
     const void* v1;
+    const void* v2p; // chain pairs (binary32 separable families), or nullptr
+    size_t (*smem_v2p)(int n, int B);
     const void* v2g; // HBM chain-state layout (large n)
     const void* v1g;
     size_t (*smem_g)(int n, int B);

@@ -1,0 +1,737 @@
+#pragma once
+// engine_kernels.cuh — kernel templates of the persistent synchronous engine
+// (V2), the asynchronous engine (V1/V0) and their per-family kernel sets.
+// Instantiated per family in engine_fam_*.cu (parallel compilation);
+// engine.cu holds the dispatch and the non-template kernels.
+//
+// Synchronous engine (engines.cpp:131-207) as ONE cooperative kernel:
+//
+//   for each level l (engines.cpp:171):
+//     every thread sweeps its chains c = gtid, gtid + G*B, ... from the
+//       level start x*_l: cache V := V*, N Metropolis trials on stream
+//       (seed, c, l) with the term-cached energy, accept bits -> masks;
+//     warp-shuffle -> block argmin -> cand[l&1][block]          (:187-190)
+//     grid.sync()
+//     every block: argmin over cand[l&1][*] (identical in all blocks), then
+//       rebuilds x*_{l+1} by replaying the winner's accepted moves from its
+//       accept mask and stream (no chain state leaves the SM), recomputes
+//       V* = cache(x*_{l+1}); block 0 keeps best-so-far and the trace
+//       (:191-198).
+//
+// One grid-wide barrier per level; cand and masks are double-buffered by
+// level parity so a block that runs ahead cannot overwrite data a slower
+// block is still reading.
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include <stdint.h>
+
+#include "engine.cuh"
+#include "engine_host.h"
+
+namespace cg = cooperative_groups;
+
+// Engine blocks never exceed 128 threads (capi.cu picks 128/64/32), and the
+// shared-memory chain state caps residency at about 4 such blocks per SM, so
+// the register budget can be 128 per thread without costing occupancy.
+#ifndef PSA_V2_MAX_THREADS
+#define PSA_V2_MAX_THREADS 128
+#endif
+#ifndef PSA_V2_MIN_BLOCKS
+#define PSA_V2_MIN_BLOCKS 4
+#endif
+
+namespace psa {
+
+// ---------------------------------------------------------------------------
+// shared-memory carve-up
+// ---------------------------------------------------------------------------
+
+struct Smem {
+    unsigned char* base;
+    size_t off = 0;
+    template <class T>
+    __device__ T* take(size_t count) {
+        off = (off + 15) & ~size_t(15);
+        T* p = reinterpret_cast<T*>(base + off);
+        off += sizeof(T) * count;
+        return p;
+    }
+};
+
+template <class R, int A>
+size_t engine_smem_bytes(int n, int B, bool rows_in_smem, bool pair = false) {
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        off = (off + 15) & ~size_t(15);
+        off += bytes;
+    };
+    if (rows_in_smem) take(sizeof(R) * size_t(row_stride<R>(pair ? 2 * n : n, A)) * B); // per-thread state rows
+    take(sizeof(double) * n);            // x*
+    take(sizeof(R) * size_t(n) * A);     // V*
+    take(sizeof(double) * n);            // lower
+    take(sizeof(double) * n);            // width
+    take(sizeof(Cand) * 34);             // reduction scratch
+    take(64);                            // scalars
+    return off;
+}
+
+struct SharedScalars {
+    double estar;
+    double best_f;
+    int32_t best_c;
+    int32_t pad;
+};
+
+template <class R, class Cost>
+__device__ void load_box(const EngineArgs& a, double* lower, double* width, Box& box) {
+    for (int k = threadIdx.x; k < a.n; k += blockDim.x) {
+        if (!a.uniform_box) {
+            lower[k] = a.lower[k];
+            width[k] = a.width[k];
+        }
+    }
+    box.lower = lower;
+    box.width = width;
+    box.lo0 = a.lo0;
+    box.w0 = a.w0;
+    box.uniform = a.uniform_box != 0;
+}
+
+// cache values of point xs (shared, n doubles) into vs (shared, n*A)
+template <class R, class Cost>
+__device__ void cache_point(const double* xs, R* vs, int n, int family) {
+    constexpr int A = Cost::A;
+    for (int k = threadIdx.x; k < n; k += blockDim.x) {
+        R t[A];
+        Cost::cache(static_cast<R>(xs[k]), k, n, t);
+#pragma unroll
+        for (int q = 0; q < A; ++q) vs[k * A + q] = t[q];
+    }
+    (void)family;
+}
+
+// The thread's chain-state row: shared memory (G = false) or HBM SoA (G = true)
+template <class R, bool G>
+struct RowSel;
+template <class R>
+struct RowSel<R, false> {
+    using T = R*;
+    static __device__ T make(R* V, int S, const EngineArgs&, size_t) { return V + static_cast<size_t>(threadIdx.x) * S; }
+};
+template <class R>
+struct RowSel<R, true> {
+    using T = StridedRow<R>;
+    static __device__ T make(R*, int, const EngineArgs& a, size_t gtid) {
+        return T{static_cast<R*>(a.rows) + gtid, a.threads};
+    }
+};
+
+// draw_random_start (engines.cpp:43-46): coordinate k uses draw k of (seed, c, 0)
+__device__ __forceinline__ double random_start_coord(const EngineArgs& a, const Box& box,
+                                                     uint32_t c, int k) {
+    const uint64_t m = draw_bits53(static_cast<uint64_t>(k), c, 0, a.keys);
+    return box.point(k, bits_to_uniform(m));
+}
+
+// Rebuild the end point of chain `cw` at level l into xs (shared), starting
+// from the level's start point already in xs.  Warp 0 only.
+static __device__ void replay_winner(const EngineArgs& a, const Box& box, double* xs, int level,
+                              int32_t cw, const uint32_t* masks) {
+    if (threadIdx.x >= 32) return;
+    const int lane = threadIdx.x;
+    const int W = (a.N + 31) / 32;
+    const uint64_t ctr0 = (level == 0 && a.random_start) ? static_cast<uint64_t>(a.n) : 0;
+    const size_t cl = static_cast<size_t>(cw - a.chain_begin);
+    for (int w = 0; w < W; ++w) {
+        const uint32_t word = masks[static_cast<size_t>(w) * a.mask_stride + cl];
+        const int j = w * 32 + lane;
+        const bool acc = j < a.N && ((word >> lane) & 1u);
+        int d = -1;
+        double xv = 0;
+        if (acc) {
+            const uint64_t base = ctr0 + 3ull * static_cast<uint64_t>(j);
+            const uint64_t m1 = draw_bits53(base, static_cast<uint32_t>(cw), level, a.keys);
+            d = coordinate_index(bits_to_uniform(m1), a.n);
+            const uint64_t m2 = draw_bits53(base + 1, static_cast<uint32_t>(cw), level, a.keys);
+            xv = box.point(d, bits_to_uniform(m2));
+        }
+        const unsigned am = __ballot_sync(0xffffffffu, acc);
+        if (acc) {
+            const unsigned same = __match_any_sync(am, d);
+            if (31 - __clz(same) == lane) xs[d] = xv; // last accepted write per coordinate
+        }
+        __syncwarp();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Multi-GPU level minloc over peer memory (NVLink / NVSwitch)
+//
+// Every GPU owns a mailbox of 2 (level parity) x world records; a record is
+// {seq, e, c, es, cs, x[n]}: the GPU's level winner (energy, global chain),
+// its start-scan winner (level 0, random starts) and the winner's end point
+// rebuilt by replay_winner.  Block 0 of each GPU stores its record into
+// every peer's mailbox (plain stores through the peer mapping, then a
+// system-scope fence and a release store of seq = epoch:level+1); every block
+// of every GPU then acquires all `world` records of the level from its own
+// mailbox and runs the same deterministic selection (better(): energy, then
+// smallest global chain), so all GPUs continue from the same x* bit for bit.
+// Parity double-buffering is safe for the same reason as cand[]: a GPU can
+// only publish level l+2 after every GPU has published level l+1, which each
+// does only after it has finished reading level l.
+// ---------------------------------------------------------------------------
+
+struct MailHeader {
+    unsigned long long seq;
+    double e;
+    int32_t c;
+    int32_t pad0;
+    double es;
+    int32_t cs;
+    int32_t pad1;
+};
+constexpr size_t kMailHeaderBytes = 48;
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+static __device__ void exchange_level(const EngineArgs& a, double* xs, Cand& w, Cand& ws, int l, Cand* scratch) {
+    const int n = a.n, tid = threadIdx.x, B = blockDim.x;
+    const size_t slot0 = static_cast<size_t>(l & 1) * a.world;
+    const unsigned long long tag = (static_cast<unsigned long long>(a.epoch) << 32) | static_cast<unsigned>(l + 1);
+    if (blockIdx.x == 0) {
+        for (int p = 0; p < a.world; ++p) {
+            char* rec = a.mail_peers[p] + (slot0 + a.rank) * a.rec_stride;
+            double* rx = reinterpret_cast<double*>(rec + kMailHeaderBytes);
+            for (int k = tid; k < n; k += B) rx[k] = xs[k];
+            if (tid == 0) {
+                MailHeader* h = reinterpret_cast<MailHeader*>(rec);
+                h->e = w.e;
+                h->c = w.c;
+                h->es = ws.e;
+                h->cs = ws.c;
+            }
+        }
+        __threadfence_system();
+        __syncthreads();
+        if (tid == 0)
+            for (int p = 0; p < a.world; ++p)
+                st_release_sys(reinterpret_cast<unsigned long long*>(a.mail_peers[p] + (slot0 + a.rank) * a.rec_stride),
+                               tag);
+    }
+    // acquire the level's records from this GPU's own mailbox
+    Cand g = empty_cand(), gs = empty_cand();
+    if (tid < a.world) {
+        const char* rec = a.mail_self + (slot0 + tid) * a.rec_stride;
+        const long long t0 = clock64();
+        while (ld_acquire_sys(reinterpret_cast<const unsigned long long*>(rec)) != tag) {
+            if (clock64() - t0 > a.spin_limit) {
+                atomicExch(a.error_flag, 1); // a peer never arrived: report instead of hanging
+                break;
+            }
+        }
+        const volatile MailHeader* h = reinterpret_cast<const volatile MailHeader*>(rec);
+        g = Cand{h->e, h->c, tid};
+        gs = Cand{h->es, h->cs, tid};
+    }
+    g = block_argmin(g, scratch);
+    if (l == 0 && a.random_start) gs = block_argmin(gs, scratch);
+    const volatile double* rx =
+        reinterpret_cast<const volatile double*>(a.mail_self + (slot0 + g.aux) * a.rec_stride + kMailHeaderBytes);
+    for (int k = tid; k < n; k += B) xs[k] = rx[k];
+    __syncthreads();
+    w = g;
+    if (l == 0 && a.random_start) ws = gs;
+}
+
+// ---------------------------------------------------------------------------
+// V2 persistent kernel
+// ---------------------------------------------------------------------------
+
+// Chain-pair traits: Cost = SepCost<float, F> runs two chains per thread
+// (sweep_pair); everything else one chain per thread (sweep).
+template <class Cost>
+struct PairOf {
+    static constexpr bool value = false;
+};
+template <template <class> class F>
+struct PairOf<SepCost<float, F>> {
+    static constexpr bool value = true;
+    template <int NT>
+    static __device__ void run(float* row, int n, float& eA, float& eB, double T, uint32_t cA, uint32_t cB,
+                               uint32_t level, uint32_t ctr, int N, const Box& box, const PhiloxKeys& keys,
+                               uint32_t* mA, uint32_t* mB, size_t ms) {
+        sweep_pair<F, NT>(row, n, eA, eB, T, cA, cB, level, ctr, N, box, keys, mA, mB, ms);
+    }
+    template <int NT>
+    static __device__ void energy(const float* row, int n, float& eA, float& eB) {
+        pair_energy<F<float>, NT>(row, n, eA, eB);
+    }
+};
+
+template <class R, class Cost, int NT, bool G, bool PAIR>
+__device__ __forceinline__ void v2_body(const EngineArgs& a) {
+    constexpr int A = Cost::A;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    cg::grid_group grid = cg::this_grid();
+    const int B = blockDim.x, tid = threadIdx.x;
+    const int n = a.n;
+    Smem sm{smem_raw};
+    // pair rows hold 2 n A interleaved values (chains A and B of the pair)
+    const int S = G ? n * A : row_stride<R>(PAIR ? 2 * n : n, A);
+    R* V = G ? nullptr : sm.take<R>(static_cast<size_t>(S) * B);
+    double* xs = sm.take<double>(n);
+    R* vs = sm.take<R>(static_cast<size_t>(n) * A);
+    double* lower = sm.take<double>(n);
+    double* width = sm.take<double>(n);
+    Cand* scratch = sm.take<Cand>(34);
+    SharedScalars* sh = sm.take<SharedScalars>(1);
+
+    Box box;
+    load_box<R, Cost>(a, lower, width, box);
+    for (int k = tid; k < n; k += B) xs[k] = a.start[k];
+    __syncthreads();
+    cache_point<R, Cost>(xs, vs, n, a.family);
+    __syncthreads();
+    if (tid == 0) {
+        sh->estar = static_cast<double>(Cost::template energy<NT>(vs, n, a.family));
+        sh->best_f = __longlong_as_double(0x7ff0000000000000ll);
+        sh->best_c = 0;
+    }
+    __syncthreads();
+
+    const size_t total_threads = static_cast<size_t>(gridDim.x) * B;
+    const size_t gtid = static_cast<size_t>(blockIdx.x) * B + tid;
+    const size_t W = static_cast<size_t>((a.N + 31) / 32);
+    const size_t mask_buf = W * a.mask_stride;
+    const auto row = RowSel<R, G>::make(V, S, a, gtid);
+    SweepStats st{0, 0};
+
+    for (int l = 0; l < a.levels; ++l) {
+        const double temperature = a.temps[l];
+        const R estar = static_cast<R>(sh->estar);
+        uint32_t* masks = a.masks + static_cast<size_t>(l & 1) * mask_buf;
+        Cand best = empty_cand(), sbest = empty_cand();
+        if constexpr (PAIR) {
+            // pair p = chains p and p + P (P = ceil(C/2)); an odd count leaves
+            // the last pair's chain B a duplicate whose results are dropped
+            // (its accept bits land in the padding columns of masks)
+            const size_t P = (a.chains_local + 1) / 2;
+            float* prow = reinterpret_cast<float*>(row);
+            for (size_t p = gtid; p < P; p += total_threads) {
+                const size_t clB = p + P;
+                const bool vB = clB < a.chains_local;
+                const uint32_t cA = static_cast<uint32_t>(a.chain_begin + p);
+                const uint32_t cB = static_cast<uint32_t>(a.chain_begin + (vB ? clB : p));
+                float eA, eB;
+                uint32_t ctr = 0;
+                if (l == 0 && a.random_start) {
+                    for (int k = 0; k < n; ++k) {
+                        float ta[A], tb[A];
+                        Cost::cache(static_cast<float>(random_start_coord(a, box, cA, k)), k, n, ta);
+                        Cost::cache(static_cast<float>(random_start_coord(a, box, cB, k)), k, n, tb);
+#pragma unroll
+                        for (int q = 0; q < A; ++q) {
+                            prow[2 * (k * A + q)] = ta[q];
+                            prow[2 * (k * A + q) + 1] = tb[q];
+                        }
+                    }
+                    PairOf<Cost>::template energy<NT>(prow, n, eA, eB);
+                    ctr = static_cast<uint32_t>(n);
+                    st.draws += static_cast<uint64_t>(n) * (vB ? 2 : 1);
+                    const Cand s1{static_cast<double>(eA), static_cast<int32_t>(cA), 0};
+                    if (better(s1, sbest)) sbest = s1;
+                    const Cand s2{static_cast<double>(eB), static_cast<int32_t>(cB), 0};
+                    if (vB && better(s2, sbest)) sbest = s2;
+                } else {
+                    unsigned long long* u = reinterpret_cast<unsigned long long*>(prow);
+                    const float* vf = reinterpret_cast<const float*>(vs);
+                    for (int e = 0; e < n * A; ++e) u[e] = f2_make(vf[e], vf[e]).v;
+                    eA = eB = static_cast<float>(estar);
+                }
+                if (l == 0) st.evals += vB ? 2 : 1; // the start evaluations (engines.cpp:157)
+                PairOf<Cost>::template run<NT>(prow, n, eA, eB, temperature, cA, cB, static_cast<uint32_t>(l), ctr,
+                                               a.N, box, a.keys, masks + p, masks + clB, a.mask_stride);
+                st.evals += static_cast<uint64_t>(a.N) * (vB ? 2 : 1);
+                st.draws += 3ull * static_cast<uint64_t>(a.N) * (vB ? 2 : 1);
+                const Cand m1{static_cast<double>(eA), static_cast<int32_t>(cA), 0};
+                if (better(m1, best)) best = m1;
+                const Cand m2{static_cast<double>(eB), static_cast<int32_t>(cB), 0};
+                if (vB && better(m2, best)) best = m2;
+            }
+        } else
+        for (size_t cl = gtid; cl < a.chains_local; cl += total_threads) {
+            const uint32_t c = static_cast<uint32_t>(a.chain_begin + cl);
+            R e;
+            uint32_t ctr = 0;
+            if (l == 0 && a.random_start) {
+                for (int k = 0; k < n; ++k) {
+                    R t[A];
+                    Cost::cache(static_cast<R>(random_start_coord(a, box, c, k)), k, n, t);
+#pragma unroll
+                    for (int q = 0; q < A; ++q) row[k * A + q] = t[q];
+                }
+                e = row_energy<Cost, NT>(row, n, a.family);
+                ctr = static_cast<uint32_t>(n);
+                st.draws += static_cast<uint64_t>(n);
+                const Cand s{static_cast<double>(e), static_cast<int32_t>(c), 0};
+                if (better(s, sbest)) sbest = s;
+            } else {
+                for (int k = 0; k < n * A; ++k) row[k] = vs[k];
+                e = estar;
+            }
+            if (l == 0) st.evals += 1; // the start evaluation (engines.cpp:157)
+            e = sweep<R, Cost, NT>(row, n, a.family, e, temperature, c, static_cast<uint32_t>(l), ctr,
+                                   a.N, box, a.keys, masks + cl, a.mask_stride, nullptr, 0, st);
+            const Cand mine{static_cast<double>(e), static_cast<int32_t>(c), 0};
+            if (better(mine, best)) best = mine;
+        }
+        // block argmin -> cand[l&1][block]
+        best = block_argmin(best, scratch);
+        if (l == 0 && a.random_start) sbest = block_argmin(sbest, scratch);
+        if (tid == 0) {
+            a.cand[static_cast<size_t>(l & 1) * gridDim.x + blockIdx.x] = best;
+            if (l == 0 && a.random_start) a.cand_start[blockIdx.x] = sbest;
+        }
+        grid.sync();
+
+        // every block: global argmin over the block candidates
+        Cand w = empty_cand(), ws = empty_cand();
+        for (int i = tid; i < static_cast<int>(gridDim.x); i += B) {
+            const Cand c = a.cand[static_cast<size_t>(l & 1) * gridDim.x + i];
+            if (better(c, w)) w = c;
+            if (l == 0 && a.random_start) {
+                const Cand s = a.cand_start[i];
+                if (better(s, ws)) ws = s;
+            }
+        }
+        w = block_argmin(w, scratch);
+        if (l == 0 && a.random_start) ws = block_argmin(ws, scratch);
+
+        // level-0 best-so-far: the start scan (engines.cpp:161-167)
+        if (l == 0 && blockIdx.x == 0) {
+            if (a.random_start) {
+                for (int k = tid; k < n; k += B) a.best_x[k] = random_start_coord(a, box, ws.c, k);
+                if (tid == 0) { sh->best_f = ws.e; sh->best_c = ws.c; }
+            } else {
+                for (int k = tid; k < n; k += B) a.best_x[k] = xs[k];
+                if (tid == 0) { sh->best_f = sh->estar; sh->best_c = 0; }
+            }
+        }
+        // the level's start point of the winner -> xs
+        if (l == 0 && a.random_start)
+            for (int k = tid; k < n; k += B) xs[k] = random_start_coord(a, box, w.c, k);
+        __syncthreads();
+        replay_winner(a, box, xs, l, w.c, masks);
+        __syncthreads();
+        if (a.world > 1) exchange_level(a, xs, w, ws, l, scratch); // the multi-GPU minloc
+        cache_point<R, Cost>(xs, vs, n, a.family);
+        __syncthreads();
+        if (tid == 0) {
+            sh->estar = w.e;
+            }
+        __syncthreads();
+        if (blockIdx.x == 0) {
+            const bool improve = w.e < sh->best_f; // engines.cpp:193 (strict)
+            if (improve)
+                for (int k = tid; k < n; k += B) a.best_x[k] = xs[k];
+            __syncthreads();
+            if (tid == 0) {
+                if (improve) {
+                    sh->best_f = w.e;
+                    sh->best_c = w.c;
+                }
+                a.trace_best[l] = sh->best_f;
+                if (a.level_winner) a.level_winner[l] = w.c;
+                if (a.level_winner_f) a.level_winner_f[l] = w.e;
+            }
+            __syncthreads();
+        }
+    }
+    if (blockIdx.x == 0 && tid == 0) {
+        a.out_scalars->best_f = sh->best_f;
+        a.out_scalars->best_chain = sh->best_c;
+    }
+    // accounting: device-side totals of evaluations and draws
+    __shared__ unsigned long long red_e, red_d;
+    if (tid == 0) { red_e = 0; red_d = 0; }
+    __syncthreads();
+    atomicAdd(&red_e, static_cast<unsigned long long>(st.evals));
+    atomicAdd(&red_d, static_cast<unsigned long long>(st.draws));
+    __syncthreads();
+    if (tid == 0) {
+        atomicAdd(&a.out_scalars->evaluations, red_e);
+        atomicAdd(&a.out_scalars->rng_draws, red_d);
+    }
+}
+
+template <class R, class Cost, int NT, bool G>
+__global__ void __launch_bounds__(PSA_V2_MAX_THREADS, PSA_V2_MIN_BLOCKS) v2_kernel(const EngineArgs a) {
+    v2_body<R, Cost, NT, G, false>(a);
+}
+
+// chain pairs: 800+ bytes of shared state per thread at n = 100 leave room
+// for 2 blocks of 128 per SM, so the register budget is 255
+template <class R, class Cost, int NT>
+__global__ void __launch_bounds__(128, 2) v2_pair_kernel(const EngineArgs a) {
+    v2_body<R, Cost, NT, false, true>(a);
+}
+
+// ---------------------------------------------------------------------------
+// V1 asynchronous kernel (engines.cpp:66-123)
+// Each thread runs whole chains through the full ladder on stream (seed,c,0).
+// Per level, the block folds its chains' running best into
+// trace_cand[l][block]; at the end each thread's best end state goes to
+// cand[gtid] with its point in xbest[gtid].  v1_finalize reduces both.
+// ---------------------------------------------------------------------------
+
+template <class R, class Cost, int NT, bool G>
+__global__ void __launch_bounds__(256) v1_kernel(const EngineArgs a) {
+    constexpr int A = Cost::A;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int B = blockDim.x, tid = threadIdx.x;
+    const int n = a.n;
+    Smem sm{smem_raw};
+    const int S = G ? n * A : row_stride<R>(n, A);
+    R* V = G ? nullptr : sm.take<R>(static_cast<size_t>(S) * B);
+    double* xs = sm.take<double>(n);
+    R* vs = sm.take<R>(static_cast<size_t>(n) * A);
+    double* lower = sm.take<double>(n);
+    double* width = sm.take<double>(n);
+    Cand* scratch = sm.take<Cand>(34);
+    SharedScalars* sh = sm.take<SharedScalars>(1);
+
+    Box box;
+    load_box<R, Cost>(a, lower, width, box);
+    for (int k = tid; k < n; k += B) xs[k] = a.start[k];
+    __syncthreads();
+    cache_point<R, Cost>(xs, vs, n, a.family);
+    __syncthreads();
+    if (tid == 0) sh->estar = static_cast<double>(Cost::template energy<NT>(vs, n, a.family));
+    __syncthreads();
+
+    const size_t total_threads = static_cast<size_t>(gridDim.x) * B;
+    const size_t gtid = static_cast<size_t>(blockIdx.x) * B + tid;
+    const size_t rounds = (a.chains_local + total_threads - 1) / total_threads;
+    const auto row = RowSel<R, G>::make(V, S, a, gtid);
+    // the chain's double-precision point: written once per accepted move, so
+    // it lives in HBM (SoA, stride = threads) and leaves shared memory to the
+    // cached terms the fold reads on every trial
+    double* xrow = a.xrows + gtid;
+    const size_t xst = a.threads;
+    SweepStats st{0, 0};
+    Cand mybest = empty_cand();
+
+    for (size_t r = 0; r < rounds; ++r) {
+        const size_t cl = gtid + r * total_threads;
+        const bool active = cl < a.chains_local;
+        const uint32_t c = static_cast<uint32_t>(a.chain_begin + cl);
+        R e = 0;
+        uint32_t ctr = 0;
+        if (active) {
+            if (a.random_start) {
+                for (int k = 0; k < n; ++k) {
+                    const double xk = random_start_coord(a, box, c, k);
+                    xrow[k * xst] = xk;
+                    R t[A];
+                    Cost::cache(static_cast<R>(xk), k, n, t);
+#pragma unroll
+                    for (int q = 0; q < A; ++q) row[k * A + q] = t[q];
+                }
+                e = row_energy<Cost, NT>(row, n, a.family);
+                ctr = static_cast<uint32_t>(n);
+                st.draws += static_cast<uint64_t>(n);
+            } else {
+                for (int k = 0; k < n; ++k) xrow[k * xst] = xs[k];
+                for (int k = 0; k < n * A; ++k) row[k] = vs[k];
+                e = static_cast<R>(sh->estar);
+            }
+            st.evals += 1;
+        }
+        double chain_best = static_cast<double>(e);
+        for (int l = 0; l < a.levels; ++l) {
+            if (active) {
+                e = sweep<R, Cost, NT>(row, n, a.family, e, a.temps[l], c, 0, ctr, a.N, box, a.keys,
+                                       nullptr, 0, xrow, xst, st);
+                ctr += 3u * static_cast<uint32_t>(a.N);
+                // std::min(chain_best, energy) (engines.cpp:94)
+                if (static_cast<double>(e) < chain_best) chain_best = static_cast<double>(e);
+            }
+            // trace: min over chains of chain_best; std::min(m, v) skips NaN and
+            // keeps the first (smallest chain) among equal values
+            Cand tv = active && !is_nan(chain_best)
+                          ? Cand{chain_best, static_cast<int32_t>(c), 0}
+                          : empty_cand();
+            tv = block_argmin(tv, scratch);
+            if (tid == 0) {
+                Cand* slot = &a.trace_cand[static_cast<size_t>(l) * gridDim.x + blockIdx.x];
+                if (r == 0 || better(tv, *slot)) *slot = tv;
+            }
+        }
+        if (active) {
+            const Cand mine{static_cast<double>(e), static_cast<int32_t>(c), static_cast<int32_t>(gtid)};
+            if (better(mine, mybest)) {
+                mybest = mine;
+                for (int k = 0; k < n; ++k)
+                    a.xbest[gtid * static_cast<size_t>(n) + k] = xrow[k * xst];
+            }
+        }
+    }
+    const Cand b = block_argmin(mybest, scratch);
+    if (tid == 0) a.cand[blockIdx.x] = b;
+
+    __shared__ unsigned long long red_e, red_d;
+    if (tid == 0) { red_e = 0; red_d = 0; }
+    __syncthreads();
+    atomicAdd(&red_e, static_cast<unsigned long long>(st.evals));
+    atomicAdd(&red_d, static_cast<unsigned long long>(st.draws));
+    __syncthreads();
+    if (tid == 0) {
+        atomicAdd(&a.out_scalars->evaluations, red_e);
+        atomicAdd(&a.out_scalars->rng_draws, red_d);
+    }
+}
+
+// f(x_i) through the engine's own cache/energy path (one point per thread)
+template <class R, class Cost>
+__global__ void probe_evaluate(const EngineArgs a, const double* x, int count, double* out) {
+    constexpr int A = Cost::A;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    R* V = reinterpret_cast<R*>(smem_raw);
+    const int B = blockDim.x;
+    R* row = V + static_cast<size_t>(threadIdx.x) * row_stride<R>(a.n, A);
+    const int i = blockIdx.x * B + threadIdx.x;
+    if (i >= count) return;
+    for (int k = 0; k < a.n; ++k) {
+        R t[A];
+        Cost::cache(static_cast<R>(x[static_cast<size_t>(i) * a.n + k]), k, a.n, t);
+#pragma unroll
+        for (int q = 0; q < A; ++q) row[k * A + q] = t[q];
+    }
+    out[i] = static_cast<double>(Cost::template energy<0>(row, a.n, a.family));
+}
+
+// metropolis_sweep (sa_core.cpp:61-79) for ONE caller-held chain — the
+// single-chain entry point of the C++ API (parsa::metropolis_sweep); the
+// engines run their own fused sweeps.  One thread walks the stream from an
+// arbitrary 64-bit counter.  The chain's cached values live in a global row;
+// every trial re-folds the whole row, so the energy is chain_energy() of the
+// point bit for bit, and the energy carried between trials is the caller's
+// double (state.energy), exactly as the reference carries it.
+template <class R, class Cost>
+__global__ void sweep_one(const EngineArgs a, double* x, R* row, double* energy,
+                          unsigned long long* counter, uint32_t chain, uint32_t level,
+                          double temperature, int n_steps) {
+    constexpr int A = Cost::A;
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const int n = a.n;
+    Box box;
+    box.lower = a.lower;
+    box.width = a.width;
+    box.lo0 = 0;
+    box.w0 = 0;
+    box.uniform = false;
+    for (int k = 0; k < n; ++k) {
+        R t[A];
+        Cost::cache(static_cast<R>(x[k]), k, n, t);
+#pragma unroll
+        for (int q = 0; q < A; ++q) row[k * A + q] = t[q];
+    }
+    double E = *energy;
+    unsigned long long ctr = *counter;
+    const float k2 = static_cast<float>(1.4426950408889634 / temperature); // log2(e) / T
+    for (int s = 0; s < n_steps; ++s) {
+        const int d = coordinate_index(bits_to_uniform(draw_bits53(ctr, chain, level, a.keys)), n);
+        const double xv = box.point(d, bits_to_uniform(draw_bits53(ctr + 1, chain, level, a.keys)));
+        const double xold = x[d];
+        R to[A], tn[A];
+        Cost::cache(static_cast<R>(xv), d, n, tn);
+#pragma unroll
+        for (int q = 0; q < A; ++q) {
+            to[q] = row[d * A + q];
+            row[d * A + q] = tn[q];
+        }
+        x[d] = xv;
+        const double trial = static_cast<double>(Cost::template energy<0>(row, n, a.family));
+        const uint64_t m3 = draw_bits53(ctr + 2, chain, level, a.keys);
+        ctr += 3;
+        int r = metropolis_fast<double>(trial, E, k2, m3);
+        if (r < 0) r = Accept<R>::exact(trial - E, temperature, m3);
+        if (r) {
+            E = trial;
+        } else {
+            x[d] = xold;
+#pragma unroll
+            for (int q = 0; q < A; ++q) row[d * A + q] = to[q];
+        }
+    }
+    *energy = E;
+    *counter = ctr;
+}
+
+// ---------------------------------------------------------------------------
+// Host-side dispatch over (precision, family)
+// ---------------------------------------------------------------------------
+
+template <class R, class Cost, int NT = 0>
+struct KernelSet {
+    static EngineKernels get() {
+        EngineKernels k;
+        k.v2 = reinterpret_cast<const void*>(&v2_kernel<R, Cost, NT, false>);
+        k.v1 = reinterpret_cast<const void*>(&v1_kernel<R, Cost, NT, false>);
+        k.v2g = reinterpret_cast<const void*>(&v2_kernel<R, Cost, 0, true>);
+        k.v1g = reinterpret_cast<const void*>(&v1_kernel<R, Cost, 0, true>);
+        k.smem_g = [](int n, int B) { return engine_smem_bytes<R, Cost::A>(n, B, false); };
+        k.state_bytes = sizeof(R) * Cost::A;
+        k.eval = reinterpret_cast<const void*>(&probe_evaluate<R, Cost>);
+        k.sweep = reinterpret_cast<const void*>(&sweep_one<R, Cost>);
+        k.smem_v2 = [](int n, int B) { return engine_smem_bytes<R, Cost::A>(n, B, true); };
+        if constexpr (PairOf<Cost>::value) {
+            k.v2p = reinterpret_cast<const void*>(&v2_pair_kernel<R, Cost, NT>);
+            k.smem_v2p = [](int n, int B) { return engine_smem_bytes<R, Cost::A>(n, B, true, true); };
+        } else {
+            k.v2p = nullptr;
+            k.smem_v2p = nullptr;
+        }
+        k.smem_v1 = [](int n, int B) { return engine_smem_bytes<R, Cost::A>(n, B, true); };
+        k.smem_eval = [](int n, int B) { return sizeof(R) * size_t(row_stride<R>(n, Cost::A)) * B; };
+        return k;
+    }
+};
+
+// Dimensions of the benchmark configurations get a compile-time n
+// (BASELINE.json: n = 10, 30, 100).
+template <class R, template <class> class F>
+EngineKernels sep_kernels(int n) {
+    switch (n) {
+    case 10: return KernelSet<R, SepCost<R, F>, 10>::get();
+    case 30: return KernelSet<R, SepCost<R, F>, 30>::get();
+    case 100: return KernelSet<R, SepCost<R, F>, 100>::get();
+    default: return KernelSet<R, SepCost<R, F>>::get();
+    }
+}
+
+// one kernel set per separable family (compile-time n for Schwefel) and one
+// for all full-evaluation families; explicit instantiations live in
+// engine_fam_*.cu
+template <class R, template <class> class F>
+EngineKernels sep_set(int n) {
+    return sep_kernels<R, F>(n);
+}
+template <class R, template <class> class F>
+EngineKernels sep_set_generic(int) {
+    return KernelSet<R, SepCost<R, F>>::get();
+}
+template <class R>
+EngineKernels full_set(int) {
+    return KernelSet<R, FullCost<R>>::get();
+}
+
+} // namespace psa
