@@ -333,7 +333,7 @@ def main():
         "gpu_launches": args.steps * plan.launches_per_run,
         "roofline": {"bound": "smem", "achieved": achieved_bw / 1e9, "peak": smem_peak / 1e9, "unit": "GB/s",
                      "frac": achieved_bw / smem_peak, "traffic": traffic,
-                     "kernel": "v2_kernel<float, SepCost<float, Schwefel>, 100> (persistent cooperative)",
+                     "kernel": plan.description + " (persistent cooperative)",
                      "algorithmic_bytes_per_trial": term_bytes, "trials_per_launch": trials_local,
                      "kernel_ms": kernel_s * 1e3, "peak_source": peak_src,
                      "traffic_note": "DRAM bytes (ncu, profiles/r01_v2_f32_ncu.json) scaled to this launch; "

@@ -208,6 +208,9 @@ psa_status psa_plan_fetch(psa_plan* p, void* cuda_stream, psa_run_result* out);
 /* number of levels, chains and device kernel launches per psa_plan_launch */
 psa_status psa_plan_info(const psa_plan* p, int32_t* levels, int32_t* chains,
                          int32_t* launches_per_run);
+/* human-readable launch description of the plan's engine kernel (layout,
+ * block, grid, shared memory), NUL-terminated into buf[capacity] */
+psa_status psa_plan_describe(const psa_plan* p, char* buf, int32_t capacity);
 psa_status psa_plan_destroy(psa_plan* p);
 /* Multi-GPU: a plan may be one rank of a `world`-GPU synchronous run.  Each
  * rank owns a mailbox in its device memory; every rank maps every peer's

@@ -550,6 +550,9 @@ class Plan:
         lv, ch, la = C.c_int32(), C.c_int32(), C.c_int32()
         _raise(self._lib, self._lib.psa_plan_info(p, C.byref(lv), C.byref(ch), C.byref(la)))
         self.levels, self.chains, self.launches_per_run = lv.value, ch.value, la.value
+        buf = C.create_string_buffer(256)
+        _raise(self._lib, self._lib.psa_plan_describe(p, buf, 256))
+        self.description = buf.value.decode()
         self._opened = []
 
     def mailbox(self) -> int:

@@ -716,6 +716,23 @@ psa_status psa_plan_info(const psa_plan* p, int32_t* levels, int32_t* chains, in
     });
 }
 
+psa_status psa_plan_describe(const psa_plan* p, char* buf, int32_t capacity) {
+    return guarded([&] {
+        if (!p || !buf || capacity < 1) fail(PSA_ERR_INVALID_ARGUMENT, "parsa_b200: null argument");
+        std::ostringstream d;
+        const char* layout = p->engine == 1 ? (p->hbm_rows ? "v1_kernel (HBM SoA rows)" : "v1_kernel (shared-memory rows)")
+                             : p->pair     ? "v2_pair_kernel (two chains per thread, shared-memory pair rows)"
+                             : p->hbm_rows ? "v2_kernel (HBM SoA rows)"
+                                           : "v2_kernel (one chain per thread, shared-memory rows)";
+        d << layout << " precision=" << (p->precision == PSA_F32 ? "f32" : "f64") << " family=" << p->family
+          << " n=" << p->n << " block=" << p->block << " grid=" << p->grid << " smem=" << p->smem;
+        const std::string t = d.str();
+        const size_t len = std::min(t.size(), static_cast<size_t>(capacity - 1));
+        std::memcpy(buf, t.data(), len);
+        buf[len] = 0;
+    });
+}
+
 psa_status psa_plan_level_detail(const psa_plan* p, int32_t* winners, double* winner_f, int32_t capacity) {
     return guarded([&] {
         if (p->engine != 2) fail(PSA_ERR_INVALID_ARGUMENT, "parsa_b200: level detail needs the synchronous engine");
