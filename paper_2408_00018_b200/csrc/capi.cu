@@ -480,13 +480,15 @@ void nm_run(const psa_objective* f, const double* x_start, const psa_nm_config* 
             fail(PSA_ERR_INVALID_ARGUMENT, "nelder_mead_minimize: infeasible start");
     require_device();
     const int max_iters = nm->max_iters > 0 ? nm->max_iters : 50000 * n;
-    DevBuf<double> d_lo, d_hi, d_x0, d_X, d_xb;
+    DevBuf<double> d_lo, d_hi, d_x0, d_X, d_Q, d_P, d_xb;
     DevBuf<psa::NMOut> d_out;
     d_lo.alloc(n);
     d_hi.alloc(n);
     d_x0.alloc(n);
     d_xb.alloc(n);
     d_X.alloc(static_cast<size_t>(n + 1) * n);
+    d_Q.alloc(static_cast<size_t>(n + 1) * n);
+    d_P.alloc(static_cast<size_t>(n + 1) * n);
     d_out.alloc(1);
     cuda_check(cudaMemcpy(d_lo.p, f->lower, sizeof(double) * n, cudaMemcpyHostToDevice), "H2D");
     cuda_check(cudaMemcpy(d_hi.p, f->upper, sizeof(double) * n, cudaMemcpyHostToDevice), "H2D");
@@ -505,6 +507,8 @@ void nm_run(const psa_objective* f, const double* x_start, const psa_nm_config* 
     a.upper = d_hi.p;
     a.x_start = d_x0.p;
     a.X = d_X.p;
+    a.Q = d_Q.p;
+    a.P = d_P.p;
     a.x_best = d_xb.p;
     a.out = d_out.p;
     const void* k = psa::nm_kernel_for(f->family);

@@ -83,7 +83,9 @@ struct NMArgsHost {
     const double* lower;
     const double* upper;
     const double* x_start;
-    double* X;      // (n+1) x n simplex storage
+    double* X;      // (n+1) x n simplex storage (vertex-major)
+    double* Q;      // (n+1) x n: Q[v][k] = X[v][k] / n, refreshed when vertex v changes
+    double* P;      // (n+1) x n: P[p][k] = centroid prefix over the first p sorted vertices
     double* x_best; // n
     NMOut* out;
 };

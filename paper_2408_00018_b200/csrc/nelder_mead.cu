@@ -1,19 +1,32 @@
 // nelder_mead.cu — device Nelder–Mead polish of the hybrid engine.
 //
 // Restates nelder_mead.cpp:37-115 (always f64) as ONE thread block that
-// runs every iteration on the device: simplex vertices in global memory
-// (row-major, (n+1) x n doubles: 2 MB at n = 500, L2-resident), the
-// centroid / trial points / cached terms in shared memory, and the simplex
-// order as an index permutation.  Each phase parallelises over coordinates
-// while keeping the reference's per-coordinate operation order:
-//   * centroid[k] += x_i[k] / n over i in sorted order (sequential per k,
-//     one IEEE division per element, nelder_mead.cpp:70-73);
-//   * each cost evaluation computes per-coordinate terms in parallel and
-//     folds them in index order on one thread (objectives.cpp semantics);
-//   * std::sort of the simplex becomes an insertion of the replaced vertex
-//     (or a full stable rank sort after a shrink) — identical order whenever
-//     the vertex values are distinct (and for any ties when n + 1 <= 16,
-//     where libstdc++'s std::sort is an insertion sort).
+// runs every iteration on the device, with the reference's results bit for
+// bit.  Simplex vertices live in global memory (vertex-major (n+1) x n
+// doubles, 2 MB at n = 500, L2-resident); the simplex order is an index
+// permutation in shared memory.
+//
+// The reference spends O(n^2) per iteration on two scans of the whole
+// simplex: the centroid (centroid[k] += x_i[k] / n over the n best vertices
+// in sorted order, one division per element, :70-73) and the diameter test
+// (:21-27).  Yet an iteration changes ONE vertex (except a shrink), so both
+// are kept incrementally, with the same floating-point operations:
+//   * Q[v][k] = x_v[k] / n is computed once when vertex v changes;
+//   * P[p/16][k] = the centroid's running sum after the first p sorted
+//     vertices, for p a multiple of 16.  Replacing the worst vertex and
+//     re-sorting leaves the order of positions < q unchanged (q = where the
+//     new vertex lands), so the sum is re-added in order from the last
+//     checkpoint at or below q (no divisions: Q is cached);
+//   * D[v] = max_k |x_v[k] - x_best[k]| per vertex, valid while the best
+//     vertex is unchanged; the diameter is the max over D (order-free).
+// A shrink, a new best vertex, or a tie-broken exact sort invalidates what
+// they touch, which is then rebuilt in full.  Each cost evaluation computes
+// the per-coordinate terms in parallel and folds them in index order on one
+// thread (objectives.cpp semantics).  std::sort becomes an insertion of the
+// replaced vertex at the position found by a parallel count (a full rank
+// sort after a shrink) — the unique sorted order when the values are
+// distinct; with ties, thread 0 runs libstdc++'s introsort itself
+// (parsa_stdsort.h).
 #include <cuda_runtime.h>
 
 #include <stdint.h>
@@ -25,6 +38,9 @@
 namespace psa {
 
 using NMArgs = NMArgsHost;
+
+// centroid prefix sums are kept at positions 0, C, 2C, ... (P row p/C)
+constexpr int kNmCheckpoint = 16;
 
 __device__ __forceinline__ double clampd(double v, double lo, double hi) {
     return v < lo ? lo : (hi < v ? hi : v); // std::clamp
@@ -54,13 +70,53 @@ __global__ void __launch_bounds__(512) nm_kernel(const NMArgs a) {
     double* xr = cen + n;
     double* xe = xr + n;
     double* xc = xe + n;
-    double* terms = xc + n;                         // n*A (A <= 2)
-    double* red = terms + 2 * static_cast<size_t>(n); // block reduction scratch (32)
-    double* scal = red + 32;                         // scalars
-    int* ord_s = reinterpret_cast<int*>(scal + 8);   // n+1
-    double* f_s = reinterpret_cast<double*>(ord_s + ((n + 1 + 1) & ~1)); // n+1
+    double* terms = xc + n;                          // n*A (A <= 2); also int scratch
+    double* red = terms + 2 * static_cast<size_t>(n) + 8; // block reduction scratch (32)
+    double* scal = red + 32;                          // scalars
+    double* f_s = scal + 8;                           // n+1 vertex values
+    double* D = f_s + (n + 1);                        // n+1 vertex diameters (vs. the best)
+    int* ord_s = reinterpret_cast<int*>(D + (n + 1)); // n+1 sorted order
+    int* ist = ord_s + (n + 1);                       // int scalars: [0] vp, [1] D owner (best id, -1 = stale)
     unsigned long long evals = 0;
     double* X = a.X;
+    double* Q = a.Q;
+    double* P = a.P;
+    const double dn = static_cast<double>(n);
+
+    // block-wide max (std::max semantics: NaN never replaces the running max)
+    auto block_max = [&](double v) {
+        for (int o = 16; o > 0; o >>= 1) {
+            const double w = __shfl_xor_sync(0xffffffffu, v, o);
+            v = v < w ? w : v;
+        }
+        if ((tid & 31) == 0) red[tid >> 5] = v;
+        __syncthreads();
+        if (tid == 0) {
+            double m = 0;
+            for (int w = 0; w < (B + 31) / 32; ++w) m = m < red[w] ? red[w] : m;
+            scal[1] = m;
+        }
+        __syncthreads();
+        const double r = scal[1];
+        __syncthreads();
+        return r;
+    };
+    // D[v] for one vertex against the current best (vertex id b)
+    auto vertex_diameter = [&](int v, int b) {
+        double d = 0;
+        for (int k = tid; k < n; k += B) {
+            const double t = fabs(X[static_cast<size_t>(v) * n + k] - X[static_cast<size_t>(b) * n + k]);
+            d = d < t ? t : d;
+        }
+        const double m = block_max(d);
+        if (tid == 0) D[v] = m;
+    };
+    auto set_vertex = [&](int v, const double* src) { // X[v] = src, Q[v] = src / n
+        for (int k = tid; k < n; k += B) {
+            X[static_cast<size_t>(v) * n + k] = src[k];
+            Q[static_cast<size_t>(v) * n + k] = src[k] / dn;
+        }
+    };
 
     // initial simplex (nelder_mead.cpp:50-59)
     for (int v = 0; v <= n; ++v) {
@@ -70,10 +126,10 @@ __global__ void __launch_bounds__(512) nm_kernel(const NMArgs a) {
                 const double step = 0.05 * (a.upper[k] - a.lower[k]);
                 xk = (xk + step <= a.upper[k]) ? xk + step : xk - step;
             }
-            X[static_cast<size_t>(v) * n + k] = xk;
             xr[k] = xk;
         }
         __syncthreads();
+        set_vertex(v, xr);
         const double fv = block_eval<Cost>(xr, n, a.family, terms, scal);
         if (tid == 0) {
             f_s[v] = fv;
@@ -81,6 +137,11 @@ __global__ void __launch_bounds__(512) nm_kernel(const NMArgs a) {
         }
         ++evals;
         __syncthreads();
+    }
+    for (int k = tid; k < n; k += B) P[k] = 0.0; // P[0] = the centroid's 0.0 fill
+    if (tid == 0) {
+        ist[0] = 0;  // valid centroid prefix length
+        ist[1] = -1; // diameters stale
     }
     // std::sort of the simplex (nelder_mead.cpp:60,111).  With pairwise
     // distinct values every correct sort yields the same order, so the block
@@ -91,7 +152,11 @@ __global__ void __launch_bounds__(512) nm_kernel(const NMArgs a) {
     int* saved = reinterpret_cast<int*>(terms) + 2 * (n + 1); // pre-sort physical order
     auto equiv = [](double a, double b) { return !(a < b) && !(b < a); };
     auto exact_sort = [&]() {
-        if (tid == 0) psa_std_sort(ord_s, n + 1, f_s);
+        if (tid == 0) {
+            psa_std_sort(ord_s, n + 1, f_s);
+            ist[0] = 0;
+            ist[1] = -1;
+        }
         __syncthreads();
     };
     auto full_sort = [&]() {
@@ -117,6 +182,11 @@ __global__ void __launch_bounds__(512) nm_kernel(const NMArgs a) {
             __syncthreads();
             exact_sort();
         }
+        if (tid == 0) {
+            ist[0] = 0;
+            ist[1] = -1;
+        }
+        __syncthreads();
     };
     full_sort();
 
@@ -124,7 +194,7 @@ __global__ void __launch_bounds__(512) nm_kernel(const NMArgs a) {
     // (shared) with value fv, then std::sort
     auto replace_worst = [&](const double* src, double fv) {
         const int w = ord_s[n];
-        for (int k = tid; k < n; k += B) X[static_cast<size_t>(w) * n + k] = src[k];
+        set_vertex(w, src);
         if (tid == 0) f_s[w] = fv;
         __syncthreads();
         int tie = 0;
@@ -136,14 +206,26 @@ __global__ void __launch_bounds__(512) nm_kernel(const NMArgs a) {
             exact_sort();
             return;
         }
+        // distinct values: the new vertex lands after every smaller value
+        int below = 0;
+        for (int p = tid; p < n; p += B) below += f_s[ord_s[p]] < fv;
+        for (int o = 16; o > 0; o >>= 1) below += __shfl_xor_sync(0xffffffffu, below, o);
+        if ((tid & 31) == 0) reinterpret_cast<int*>(red)[tid >> 5] = below;
+        __syncthreads();
+        int pos = 0;
+        for (int i = 0; i < (B + 31) / 32; ++i) pos += reinterpret_cast<int*>(red)[i];
+        __syncthreads();
+        // shift ord[pos..n-1] up by one and insert w at pos
+        for (int p = tid; p <= n; p += B) saved[p] = ord_s[p];
+        __syncthreads();
+        for (int p = pos + 1 + tid; p <= n; p += B) ord_s[p] = saved[p - 1];
         if (tid == 0) {
-            int p = n;
-            while (p > 0 && fv < f_s[ord_s[p - 1]]) {
-                ord_s[p] = ord_s[p - 1];
-                --p;
-            }
-            ord_s[p] = w;
+            ord_s[pos] = w;
+            if (pos < ist[0]) ist[0] = pos;  // centroid prefixes before pos stay valid
+            if (pos == 0) ist[1] = -1;       // a new best: every diameter is stale
         }
+        __syncthreads();
+        if (pos > 0 && ist[1] >= 0) vertex_diameter(w, ord_s[0]);
         __syncthreads();
     };
 
@@ -151,34 +233,46 @@ __global__ void __launch_bounds__(512) nm_kernel(const NMArgs a) {
     for (; iter < a.max_iters; ++iter) {
         // termination (nelder_mead.cpp:67-68; simplex_diameter :21-27)
         const int b0 = ord_s[0];
-        double dmax = 0;
-        for (int k = tid; k < n; k += B) {
-            const double x0 = X[static_cast<size_t>(b0) * n + k];
-            for (int i = 1; i <= n; ++i) {
-                const double d = fabs(X[static_cast<size_t>(ord_s[i]) * n + k] - x0);
-                dmax = dmax < d ? d : dmax;
+        if (ist[1] != b0) {
+            // all diameters against the best: one warp per vertex
+            const int lane = tid & 31, warp = tid >> 5, nw = B >> 5;
+            for (int v = warp; v <= n; v += nw) {
+                double d = 0;
+                for (int k = lane; k < n; k += 32) {
+                    const double t = fabs(X[static_cast<size_t>(v) * n + k] - X[static_cast<size_t>(b0) * n + k]);
+                    d = d < t ? t : d;
+                }
+                for (int o = 16; o > 0; o >>= 1) {
+                    const double w = __shfl_xor_sync(0xffffffffu, d, o);
+                    d = d < w ? w : d;
+                }
+                if (lane == 0) D[v] = d;
             }
+            __syncthreads();
+            if (tid == 0) ist[1] = b0;
+            __syncthreads();
         }
-        for (int o = 16; o > 0; o >>= 1) {
-            const double w = __shfl_xor_sync(0xffffffffu, dmax, o);
-            dmax = dmax < w ? w : dmax;
-        }
-        if ((tid & 31) == 0) red[tid >> 5] = dmax;
-        __syncthreads();
-        if (tid == 0) {
-            double m = 0;
-            for (int w = 0; w < (B + 31) / 32; ++w) m = m < red[w] ? red[w] : m;
-            scal[1] = m;
-        }
-        __syncthreads();
-        if (f_s[ord_s[n]] - f_s[ord_s[0]] <= a.f_tol || scal[1] <= a.x_tol) break;
+        double dm = 0;
+        for (int i = 1 + tid; i <= n; i += B) dm = dm < D[ord_s[i]] ? D[ord_s[i]] : dm;
+        const double dmax = block_max(dm);
+        if (f_s[ord_s[n]] - f_s[ord_s[0]] <= a.f_tol || dmax <= a.x_tol) break;
 
-        // centroid of the n best (nelder_mead.cpp:70-73)
+        // centroid of the n best (nelder_mead.cpp:70-73): re-add from the
+        // first position whose vertex changed
+        // (prefixes are stored every kNmCheckpoint positions: re-adding from
+        // the checkpoint at or below the first changed position costs a few
+        // adds, storing every prefix would cost an O(n^2) write stream)
+        const int vp = (ist[0] / kNmCheckpoint) * kNmCheckpoint;
         for (int k = tid; k < n; k += B) {
-            double c = 0.0;
-            for (int i = 0; i < n; ++i) c += X[static_cast<size_t>(ord_s[i]) * n + k] / n;
+            double c = P[static_cast<size_t>(vp / kNmCheckpoint) * n + k];
+            for (int p = vp; p < n; ++p) {
+                c += Q[static_cast<size_t>(ord_s[p]) * n + k];
+                if ((p + 1) % kNmCheckpoint == 0) P[static_cast<size_t>((p + 1) / kNmCheckpoint) * n + k] = c;
+            }
             cen[k] = c;
         }
+        __syncthreads();
+        if (tid == 0) ist[0] = n;
         const int worst = ord_s[n];
         const double worst_f = f_s[worst];
         for (int k = tid; k < n; k += B) {
@@ -217,11 +311,10 @@ __global__ void __launch_bounds__(512) nm_kernel(const NMArgs a) {
                     for (int k = tid; k < n; k += B) {
                         const double x0 = X[static_cast<size_t>(best) * n + k];
                         const double xv = X[static_cast<size_t>(v) * n + k];
-                        const double nv = clampd(x0 + a.shrink * (xv - x0), a.lower[k], a.upper[k]);
-                        X[static_cast<size_t>(v) * n + k] = nv;
-                        xr[k] = nv;
+                        xr[k] = clampd(x0 + a.shrink * (xv - x0), a.lower[k], a.upper[k]);
                     }
                     __syncthreads();
+                    set_vertex(v, xr);
                     const double fv = block_eval<Cost>(xr, n, a.family, terms, scal);
                     ++evals;
                     if (tid == 0) f_s[v] = fv;
@@ -243,9 +336,10 @@ __global__ void __launch_bounds__(512) nm_kernel(const NMArgs a) {
 
 size_t nm_smem_bytes(int n) {
     // cen, xr, xe, xc (4n) + terms (2n, also int scratch for 3(n+1) ids) +
-    // reduction/scalars (40) + order (n+1 ints) + values (n+1)
-    return sizeof(double) * (6 * static_cast<size_t>(n) + 48) + sizeof(int) * (n + 3) +
-           sizeof(double) * (n + 2) + 64;
+    // reduction/scalars (40) + values and diameters (2(n+1)) + order (n+1
+    // ints) + int scalars
+    return sizeof(double) * (6 * static_cast<size_t>(n) + 48 + 2 * (static_cast<size_t>(n) + 1)) +
+           sizeof(int) * (n + 1 + 4) + 64;
 }
 
 template <class Cost>
