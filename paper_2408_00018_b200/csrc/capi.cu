@@ -276,14 +276,30 @@ void plan_build(psa_plan* p, const psa_objective* f, const psa_engine_config* cf
     const char* mode_env = std::getenv("PSA_V2_MODE");
     const std::string mode = mode_env ? mode_env : "";
     const char* no_pair = std::getenv("PSA_NO_PAIR");
-    if (engine == 2 && !p->hbm_rows && p->ks.v2p && mode != "single" && !(no_pair && no_pair[0] == '1')) {
+    // Pairs halve the threads for the same chains, so they pay off only when
+    // the pair kernel still keeps >= 8 warps per SM resident and there are
+    // enough pairs to fill them (small chain counts or large n keep one chain
+    // per thread; PSA_V2_MODE=pair forces pairs whenever the rows fit).
+    const void* pair_kern = engine == 2 ? p->ks.v2p : p->ks.v1p;
+    if (!p->hbm_rows && pair_kern && mode != "single" && !(no_pair && no_pair[0] == '1')) {
         int Bp = 128;
         while (Bp > 32 && p->ks.smem_v2p(n, Bp) > smem_cap) Bp /= 2;
-        if (p->ks.smem_v2p(n, Bp) <= smem_cap) {
-            p->pair = true;
-            p->block = B = Bp;
-            p->smem = p->ks.smem_v2p(n, Bp);
-            kern = p->ks.v2p;
+        const size_t smem_p = p->ks.smem_v2p(n, Bp);
+        if (smem_p <= smem_cap) {
+            cuda_check(cudaFuncSetAttribute(pair_kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            static_cast<int>(smem_p)),
+                       "cudaFuncSetAttribute");
+            int per_sm_p = 0;
+            cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_p, pair_kern, Bp, smem_p), "occupancy");
+            const long long pair_threads = static_cast<long long>(per_sm_p) * Bp * prop.multiProcessorCount;
+            const long long pairs = (static_cast<long long>(p->chains_local) + 1) / 2;
+            const bool worth = per_sm_p * Bp >= 256 && pairs >= pair_threads;
+            if (worth || mode == "pair") {
+                p->pair = true;
+                p->block = B = Bp;
+                p->smem = smem_p;
+                kern = pair_kern;
+            }
         }
     }
     p->kernel = kern;
@@ -322,7 +338,7 @@ void plan_build(psa_plan* p, const psa_objective* f, const psa_engine_config* cf
         p->d_cand.alloc(p->grid);
         p->d_trace_cand.alloc(static_cast<size_t>(p->levels) * p->grid);
         p->d_xbest.alloc(static_cast<size_t>(p->grid) * B * n);
-        p->d_xrows.alloc(static_cast<size_t>(p->grid) * B * n);
+        p->d_xrows.alloc((p->pair ? 2 : 1) * static_cast<size_t>(p->grid) * B * n);
     }
     const size_t threads = static_cast<size_t>(p->grid) * B;
     if (p->hbm_rows) p->d_rows.alloc(threads * static_cast<size_t>(n) * p->ks.state_bytes);
@@ -724,7 +740,9 @@ psa_status psa_plan_describe(const psa_plan* p, char* buf, int32_t capacity) {
     return guarded([&] {
         if (!p || !buf || capacity < 1) fail(PSA_ERR_INVALID_ARGUMENT, "parsa_b200: null argument");
         std::ostringstream d;
-        const char* layout = p->engine == 1 ? (p->hbm_rows ? "v1_kernel (HBM SoA rows)" : "v1_kernel (shared-memory rows)")
+        const char* layout = p->engine == 1 ? (p->pair       ? "v1_pair_kernel (two chains per thread, shared-memory pair rows)"
+                                               : p->hbm_rows ? "v1_kernel (HBM SoA rows)"
+                                                             : "v1_kernel (shared-memory rows)")
                              : p->pair     ? "v2_pair_kernel (two chains per thread, shared-memory pair rows)"
                              : p->hbm_rows ? "v2_kernel (HBM SoA rows)"
                                            : "v2_kernel (one chain per thread, shared-memory rows)";

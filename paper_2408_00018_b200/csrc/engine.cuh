@@ -472,10 +472,13 @@ PSA_DEV void pair_energy(const float* row, int n_rt, float& eA, float& eB) {
 // sweep() of sa_core.cpp:61-79 for two chains at once.  Each chain's draws,
 // proposals, energies and decisions are exactly those of sweep(); only the
 // fold is shared (FADD2).  Accept bits go to maskA/maskB[w * mask_stride].
+// (V1 passes no masks and the chains' double-precision points xa/xb, which
+// accepted moves update, x[k * xs].)
 template <template <class> class F, int NT>
 PSA_DEV void sweep_pair(float* row, int n_rt, float& EA, float& EB, double temperature, uint32_t cA,
                         uint32_t cB, uint32_t level, uint32_t ctr, int N, const Box& box, const PhiloxKeys& keys,
-                        uint32_t* maskA, uint32_t* maskB, size_t mask_stride) {
+                        uint32_t* maskA, uint32_t* maskB, size_t mask_stride, double* xa = nullptr,
+                        double* xb = nullptr, size_t xs = 0) {
     using Fam = F<float>;
     using Cost = SepCost<float, F>;
     constexpr int A = Fam::kArrays;
@@ -548,27 +551,33 @@ PSA_DEV void sweep_pair(float* row, int n_rt, float& EA, float& EB, double tempe
         EB = rB ? trB : EB;
         wordA |= static_cast<uint32_t>(rA) << (j & 31);
         wordB |= static_cast<uint32_t>(rB) << (j & 31);
+        if (xa) {
+            if (rA) xa[static_cast<size_t>(dA) * xs] = xA;
+            if (rB) xb[static_cast<size_t>(dB) * xs] = xB;
+        }
 #pragma unroll
         for (int a = 0; a < A; ++a) {
             if (!rA) row[2 * (dA * A + a)] = oA[a];
             if (!rB) row[2 * (dB * A + a) + 1] = oB[a];
         }
         if ((j & 31) == 31 || j == N - 1) {
-            maskA[static_cast<size_t>(j >> 5) * mask_stride] = wordA;
-            maskB[static_cast<size_t>(j >> 5) * mask_stride] = wordB;
+            if (maskA) {
+                maskA[static_cast<size_t>(j >> 5) * mask_stride] = wordA;
+                maskB[static_cast<size_t>(j >> 5) * mask_stride] = wordB;
+            }
             wordA = 0;
             wordB = 0;
         }
         dA = nA;
         dB = nB;
+        xA = yA;
+        xB = yB;
 #pragma unroll
         for (int a = 0; a < A; ++a) {
             tA[a] = uA[a];
             tB[a] = uB[a];
         }
     }
-    (void)xA;
-    (void)xB;
 }
 
 // ---------------------------------------------------------------------------

@@ -6,10 +6,10 @@
 
 namespace psa {
 
-template EngineKernels sep_set_generic<float, Ackley>(int);
+template EngineKernels sep_set<float, Ackley>(int);
 template EngineKernels sep_set_generic<float, CosineMixture>(int);
 template EngineKernels sep_set_generic<float, Exponential>(int);
-template EngineKernels sep_set_generic<double, Ackley>(int);
+template EngineKernels sep_set<double, Ackley>(int);
 template EngineKernels sep_set_generic<double, CosineMixture>(int);
 template EngineKernels sep_set_generic<double, Exponential>(int);
 

@@ -6,12 +6,12 @@
 
 namespace psa {
 
-template EngineKernels sep_set_generic<float, Griewank>(int);
+template EngineKernels sep_set<float, Griewank>(int);
 template EngineKernels sep_set_generic<float, Michalewicz>(int);
-template EngineKernels sep_set_generic<float, Rastrigin>(int);
-template EngineKernels sep_set_generic<double, Griewank>(int);
+template EngineKernels sep_set<float, Rastrigin>(int);
+template EngineKernels sep_set<double, Griewank>(int);
 template EngineKernels sep_set_generic<double, Michalewicz>(int);
-template EngineKernels sep_set_generic<double, Rastrigin>(int);
+template EngineKernels sep_set<double, Rastrigin>(int);
 
 } // namespace psa
 #endif

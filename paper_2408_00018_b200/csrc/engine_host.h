@@ -43,7 +43,7 @@ struct EngineArgs {
     uint32_t chain_begin;  // global index of the shard's first chain
     uint32_t chains_total;
     void* rows;            // HBM layout only: [n*A][threads] chain state (R elements)
-    double* xrows;         // V1: [n][threads] double-precision point of each thread's chain
+    double* xrows;         // V1: [n][threads] point of each thread's chain ([2][n][threads] for pairs)
     size_t threads;        // grid * block (the SoA stride of rows/xrows)
     uint32_t* masks;       // V2: [2][ceil(N/32)][mask_stride] accept bits
     size_t mask_stride;    // chains_local, rounded up to even (chain pairs)
@@ -94,7 +94,8 @@ struct EngineKernels {
     const void* v2;
     const void* v1;
     const void* v2p; // chain pairs (binary32 separable families), or nullptr
-    size_t (*smem_v2p)(int n, int B);
+    const void* v1p; // V1 with chain pairs, or nullptr
+    size_t (*smem_v2p)(int n, int B); // pair rows (the same for V1 pairs)
     const void* v2g; // HBM chain-state layout (large n)
     const void* v1g;
     size_t (*smem_g)(int n, int B);

@@ -271,6 +271,12 @@ struct PairOf<SepCost<float, F>> {
         sweep_pair<F, NT>(row, n, eA, eB, T, cA, cB, level, ctr, N, box, keys, mA, mB, ms);
     }
     template <int NT>
+    static __device__ void run_x(float* row, int n, float& eA, float& eB, double T, uint32_t cA, uint32_t cB,
+                                 uint32_t ctr, int N, const Box& box, const PhiloxKeys& keys, double* xa, double* xb,
+                                 size_t xs) {
+        sweep_pair<F, NT>(row, n, eA, eB, T, cA, cB, 0u, ctr, N, box, keys, nullptr, nullptr, 0, xa, xb, xs);
+    }
+    template <int NT>
     static __device__ void energy(const float* row, int n, float& eA, float& eB) {
         pair_energy<F<float>, NT>(row, n, eA, eB);
     }
@@ -599,6 +605,135 @@ __global__ void __launch_bounds__(256) v1_kernel(const EngineArgs a) {
     }
 }
 
+// V1 with chain pairs (binary32 separable families): thread t runs chains p
+// and p + P (P = ceil(C/2)) through the whole ladder side by side
+// (sweep_pair), each on its own stream (seed, c, 0); per level the block
+// folds both chains' running best into the trace candidate.  Points live in
+// HBM, one SoA row per chain of the pair (xrows[2][n][threads]).
+template <class R, class Cost, int NT>
+__global__ void __launch_bounds__(128, 3) v1_pair_kernel(const EngineArgs a) {
+    constexpr int A = Cost::A;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int B = blockDim.x, tid = threadIdx.x;
+    const int n = a.n;
+    Smem sm{smem_raw};
+    const int S = row_stride<float>(2 * n, A);
+    float* V = sm.take<float>(static_cast<size_t>(S) * B);
+    double* xs = sm.take<double>(n);
+    float* vs = sm.take<float>(static_cast<size_t>(n) * A);
+    double* lower = sm.take<double>(n);
+    double* width = sm.take<double>(n);
+    Cand* scratch = sm.take<Cand>(34);
+    SharedScalars* sh = sm.take<SharedScalars>(1);
+
+    Box box;
+    load_box<float, Cost>(a, lower, width, box);
+    for (int k = tid; k < n; k += B) xs[k] = a.start[k];
+    __syncthreads();
+    cache_point<float, Cost>(xs, vs, n, a.family);
+    __syncthreads();
+    if (tid == 0) sh->estar = static_cast<double>(Cost::template energy<NT>(vs, n, a.family));
+    __syncthreads();
+
+    const size_t total_threads = static_cast<size_t>(gridDim.x) * B;
+    const size_t gtid = static_cast<size_t>(blockIdx.x) * B + tid;
+    const size_t P = (a.chains_local + 1) / 2;
+    const size_t rounds = (P + total_threads - 1) / total_threads;
+    float* row = V + static_cast<size_t>(tid) * S;
+    const size_t xst = a.threads;
+    double* xa = a.xrows + gtid;
+    double* xb = a.xrows + static_cast<size_t>(n) * xst + gtid;
+    SweepStats st{0, 0};
+    Cand mybest = empty_cand();
+
+    for (size_t r = 0; r < rounds; ++r) {
+        const size_t p = gtid + r * total_threads;
+        const bool active = p < P;
+        const bool vB = p + P < a.chains_local;
+        const uint32_t cA = static_cast<uint32_t>(a.chain_begin + p);
+        const uint32_t cB = static_cast<uint32_t>(a.chain_begin + (vB ? p + P : p));
+        float eA = 0, eB = 0;
+        uint32_t ctr = 0;
+        if (active) {
+            if (a.random_start) {
+                for (int k = 0; k < n; ++k) {
+                    const double ya = random_start_coord(a, box, cA, k), yb = random_start_coord(a, box, cB, k);
+                    xa[k * xst] = ya;
+                    xb[k * xst] = yb;
+                    float ta[A], tb[A];
+                    Cost::cache(static_cast<float>(ya), k, n, ta);
+                    Cost::cache(static_cast<float>(yb), k, n, tb);
+#pragma unroll
+                    for (int q = 0; q < A; ++q) {
+                        row[2 * (k * A + q)] = ta[q];
+                        row[2 * (k * A + q) + 1] = tb[q];
+                    }
+                }
+                PairOf<Cost>::template energy<NT>(row, n, eA, eB);
+                ctr = static_cast<uint32_t>(n);
+                st.draws += static_cast<uint64_t>(n) * (vB ? 2 : 1);
+            } else {
+                for (int k = 0; k < n; ++k) {
+                    xa[k * xst] = xs[k];
+                    xb[k * xst] = xs[k];
+                }
+                unsigned long long* u = reinterpret_cast<unsigned long long*>(row);
+                for (int e = 0; e < n * A; ++e) u[e] = f2_make(vs[e], vs[e]).v;
+                eA = eB = static_cast<float>(sh->estar);
+            }
+            st.evals += vB ? 2 : 1;
+        }
+        double bestA = eA, bestB = eB;
+        for (int l = 0; l < a.levels; ++l) {
+            if (active) {
+                PairOf<Cost>::template run_x<NT>(row, n, eA, eB, a.temps[l], cA, cB, ctr, a.N, box, a.keys, xa, xb,
+                                                 xst);
+                ctr += 3u * static_cast<uint32_t>(a.N);
+                st.evals += static_cast<uint64_t>(a.N) * (vB ? 2 : 1);
+                st.draws += 3ull * static_cast<uint64_t>(a.N) * (vB ? 2 : 1);
+                // std::min(chain_best, energy) (engines.cpp:94)
+                if (static_cast<double>(eA) < bestA) bestA = eA;
+                if (static_cast<double>(eB) < bestB) bestB = eB;
+            }
+            // trace: min over chains of the running best (std::min skips NaN
+            // and keeps the smallest chain among equal values)
+            Cand tv = active && !is_nan(bestA) ? Cand{bestA, static_cast<int32_t>(cA), 0} : empty_cand();
+            const Cand tb = active && vB && !is_nan(bestB) ? Cand{bestB, static_cast<int32_t>(cB), 0} : empty_cand();
+            if (better(tb, tv)) tv = tb;
+            tv = block_argmin(tv, scratch);
+            if (tid == 0) {
+                Cand* slot = &a.trace_cand[static_cast<size_t>(l) * gridDim.x + blockIdx.x];
+                if (r == 0 || better(tv, *slot)) *slot = tv;
+            }
+        }
+        if (active) {
+            const Cand ma{static_cast<double>(eA), static_cast<int32_t>(cA), static_cast<int32_t>(gtid)};
+            if (better(ma, mybest)) {
+                mybest = ma;
+                for (int k = 0; k < n; ++k) a.xbest[gtid * static_cast<size_t>(n) + k] = xa[k * xst];
+            }
+            const Cand mb{static_cast<double>(eB), static_cast<int32_t>(cB), static_cast<int32_t>(gtid)};
+            if (vB && better(mb, mybest)) {
+                mybest = mb;
+                for (int k = 0; k < n; ++k) a.xbest[gtid * static_cast<size_t>(n) + k] = xb[k * xst];
+            }
+        }
+    }
+    const Cand b = block_argmin(mybest, scratch);
+    if (tid == 0) a.cand[blockIdx.x] = b;
+
+    __shared__ unsigned long long red_e, red_d;
+    if (tid == 0) { red_e = 0; red_d = 0; }
+    __syncthreads();
+    atomicAdd(&red_e, static_cast<unsigned long long>(st.evals));
+    atomicAdd(&red_d, static_cast<unsigned long long>(st.draws));
+    __syncthreads();
+    if (tid == 0) {
+        atomicAdd(&a.out_scalars->evaluations, red_e);
+        atomicAdd(&a.out_scalars->rng_draws, red_d);
+    }
+}
+
 // f(x_i) through the engine's own cache/energy path (one point per thread)
 template <class R, class Cost>
 __global__ void probe_evaluate(const EngineArgs a, const double* x, int count, double* out) {
@@ -694,9 +829,11 @@ struct KernelSet {
         k.sweep = reinterpret_cast<const void*>(&sweep_one<R, Cost>);
         k.smem_v2 = [](int n, int B) { return engine_smem_bytes<R, Cost::A>(n, B, true); };
         if constexpr (PairOf<Cost>::value) {
+            k.v1p = reinterpret_cast<const void*>(&v1_pair_kernel<R, Cost, NT>);
             k.v2p = reinterpret_cast<const void*>(&v2_pair_kernel<R, Cost, NT>);
             k.smem_v2p = [](int n, int B) { return engine_smem_bytes<R, Cost::A>(n, B, true, true); };
         } else {
+            k.v1p = nullptr;
             k.v2p = nullptr;
             k.smem_v2p = nullptr;
         }
