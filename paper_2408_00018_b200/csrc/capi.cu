@@ -528,11 +528,38 @@ void nm_run(const psa_objective* f, const double* x_start, const psa_nm_config* 
     a.x_best = d_xb.p;
     a.out = d_out.p;
     const void* k = psa::nm_kernel_for(f->family);
-    const size_t smem = psa::nm_smem_bytes(n);
+    // one thread-block cluster: CTA r owns ~32 coordinate columns (up to 16
+    // CTAs, the non-portable cluster size of sm_100)
+    int cl_max = 16;
+    if (const char* e = std::getenv("PSA_NM_CLUSTER")) cl_max = std::max(1, std::min(16, std::atoi(e)));
+    const int cl = std::max(1, std::min(cl_max, (n + 31) / 32));
+    int dev = 0;
+    cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+    int smem_cap = 0;
+    cuda_check(cudaDeviceGetAttribute(&smem_cap, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev), "attribute");
+    a.q_smem = psa::nm_smem_bytes(n, cl, true) <= static_cast<size_t>(smem_cap) ? 1 : 0;
+    const size_t smem = psa::nm_smem_bytes(n, cl, a.q_smem != 0);
     cuda_check(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
                "cudaFuncSetAttribute");
+    if (cl > 8)
+        cuda_check(cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
+                   "cudaFuncSetAttribute(non-portable cluster)");
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3(cl);
+    int nm_block = 512;
+    if (const char* e = std::getenv("PSA_NM_BLOCK")) nm_block = std::max(32, std::min(512, std::atoi(e) / 32 * 32));
+    lc.blockDim = dim3(nm_block);
+    lc.dynamicSmemBytes = smem;
+    lc.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cl;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
     void* params[] = {&a};
-    cuda_check(cudaLaunchKernel(k, dim3(1), dim3(n >= 256 ? 512 : 128), params, smem, stream), "launch nm_kernel");
+    cuda_check(cudaLaunchKernelExC(&lc, k, params), "launch nm_kernel");
     psa::NMOut o;
     cuda_check(cudaMemcpyAsync(&o, d_out.p, sizeof(o), cudaMemcpyDeviceToHost, stream), "D2H");
     if (out->x_best)

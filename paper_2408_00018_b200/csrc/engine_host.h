@@ -78,7 +78,7 @@ struct NMArgsHost {
     int n;
     int family;
     int max_iters;
-    int pad;
+    int q_smem; // 1: each CTA keeps its columns of Q and P in shared memory
     double reflect, expand, contract, shrink, f_tol, x_tol;
     const double* lower;
     const double* upper;
@@ -113,7 +113,7 @@ const void* probe_philox_kernel();
 const void* v1_finalize_kernel();
 const void* probe_libm_f32_kernel();
 const void* nm_kernel_for(int family);
-size_t nm_smem_bytes(int n);
+size_t nm_smem_bytes(int n, int cluster_ctas, bool q_smem);
 const void* probe_libm_f64_kernel();
 
 } // namespace psa

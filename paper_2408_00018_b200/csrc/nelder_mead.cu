@@ -27,6 +27,7 @@
 // sort after a shrink) — the unique sorted order when the values are
 // distinct; with ties, thread 0 runs libstdc++'s introsort itself
 // (parsa_stdsort.h).
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <stdint.h>
@@ -37,6 +38,8 @@
 
 namespace psa {
 
+namespace cg = cooperative_groups;
+
 using NMArgs = NMArgsHost;
 
 // centroid prefix sums are kept at positions 0, C, 2C, ... (P row p/C)
@@ -46,43 +49,82 @@ __device__ __forceinline__ double clampd(double v, double lo, double hi) {
     return v < lo ? lo : (hi < v ? hi : v); // std::clamp
 }
 
-// f64 evaluation of the shared-memory point xs (block-cooperative)
-template <class Cost>
-__device__ double block_eval(const double* xs, int n, int family, double* terms, double* result) {
-    constexpr int A = Cost::A;
-    for (int k = threadIdx.x; k < n; k += blockDim.x) {
-        double t[A];
-        Cost::cache(xs[k], k, n, t);
-#pragma unroll
-        for (int a = 0; a < A; ++a) terms[k * A + a] = t[a];
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) *result = Cost::template energy<0>(terms, n, family);
-    __syncthreads();
-    return *result;
-}
+// ---------------------------------------------------------------------------
+// One Nelder–Mead instance on a thread-block CLUSTER of CL CTAs (CL = 1 for
+// small n).  CTA r owns the coordinate columns [c0, c1): it keeps its slice
+// of the simplex (X, Q, P in global memory), of the centroid and of the trial
+// points, and computes those columns' cost terms.  The cost fold needs every
+// term in index order, so the terms are gathered into CTA 0's shared memory
+// (DSMEM stores), CTA 0 folds them on one thread and stores the value into
+// every CTA (two cluster barriers per evaluation).  Everything that decides
+// the control flow — the values f, the sorted order, ties, insertion points —
+// is replicated in every CTA and updated by the same operations on the same
+// data, so every CTA takes the same branches.  The simplex diameter is a max
+// over columns, so each CTA keeps per-vertex maxima over its own columns and
+// the termination test max-reduces CL partials through DSMEM.
+// ---------------------------------------------------------------------------
 
 template <class Cost>
 __global__ void __launch_bounds__(512) nm_kernel(const NMArgs a) {
+    constexpr int A = Cost::A;
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    cg::cluster_group cluster = cg::this_cluster();
+    const int CL = static_cast<int>(cluster.num_blocks());
+    const int rank = static_cast<int>(cluster.block_rank());
     const int n = a.n, tid = threadIdx.x, B = blockDim.x;
-    double* cen = reinterpret_cast<double*>(smem_raw);
-    double* xr = cen + n;
-    double* xe = xr + n;
-    double* xc = xe + n;
-    double* terms = xc + n;                          // n*A (A <= 2); also int scratch
-    double* red = terms + 2 * static_cast<size_t>(n) + 8; // block reduction scratch (32)
-    double* scal = red + 32;                          // scalars
-    double* f_s = scal + 8;                           // n+1 vertex values
-    double* D = f_s + (n + 1);                        // n+1 vertex diameters (vs. the best)
-    int* ord_s = reinterpret_cast<int*>(D + (n + 1)); // n+1 sorted order
-    int* ist = ord_s + (n + 1);                       // int scalars: [0] vp, [1] D owner (best id, -1 = stale)
+    const int c0 = static_cast<int>((static_cast<long long>(rank) * n) / CL);
+    const int c1 = static_cast<int>((static_cast<long long>(rank + 1) * n) / CL);
+    const int nc = c1 - c0; // columns of this CTA
+    // every CTA uses the same shared-memory layout (sized for the widest
+    // column slice), so DSMEM addresses mapped from local pointers line up
+    const int ncmax = (n + CL - 1) / CL;
+
+    double* terms = reinterpret_cast<double*>(smem_raw);  // n*A: the gather target in CTA 0
+    double* cen = terms + 2 * static_cast<size_t>(n) + 8;  // own columns
+    double* xr = cen + ncmax;
+    double* xe = xr + ncmax;
+    double* xc = xe + ncmax;
+    double* red = xc + ncmax;                               // block reduction scratch (32)
+    double* scal = red + 32;                                // scalars: [0] broadcast f, [1] block max
+    double* dslot = scal + 8;                               // CL diameter partials (<= 16)
+    double* f_s = dslot + 16;                               // n+1 vertex values
+    double* D = f_s + (n + 1);                              // n+1 vertex diameters over own columns
+    int* ord_s = reinterpret_cast<int*>(D + (n + 1));       // n+1 sorted order
+    int* ist = ord_s + (n + 1);                             // int scalars: [0] vp, [1] D owner (-1 = stale)
     unsigned long long evals = 0;
     double* X = a.X;
-    double* Q = a.Q;
-    double* P = a.P;
+    // Q (and the centroid checkpoints P) of this CTA's columns: in shared
+    // memory when the slice fits (a.q_smem), else in global memory.  Element
+    // (v, j) of either lives at base[v * stride + j].
+    // (the shared slice starts after the int scratch: ist[4], ranks, saved order)
+    const uintptr_t qraw = (reinterpret_cast<uintptr_t>(ist + 4 + 2 * (n + 1)) + 15) & ~uintptr_t(15);
+    double* Qb = a.q_smem ? reinterpret_cast<double*>(qraw) : a.Q + c0;
+    const size_t qst = a.q_smem ? static_cast<size_t>(ncmax) : static_cast<size_t>(n);
+    double* Pb = a.q_smem ? Qb + static_cast<size_t>(n + 1) * ncmax : a.P + c0;
     const double dn = static_cast<double>(n);
+    double* terms0 = cluster.map_shared_rank(terms, 0);
+    // cluster barrier (a plain block barrier when the cluster is one CTA)
+    auto csync = [&]() {
+        if (CL == 1) __syncthreads();
+        else cluster.sync();
+    };
 
+    // f(x) for the point whose own columns are in xs (every CTA calls this)
+    auto eval = [&](const double* xs) {
+        for (int j = tid; j < nc; j += B) {
+            double t[A];
+            Cost::cache(xs[j], c0 + j, n, t);
+#pragma unroll
+            for (int q = 0; q < A; ++q) terms0[static_cast<size_t>(c0 + j) * A + q] = t[q];
+        }
+        csync();
+        if (rank == 0 && tid == 0) {
+            const double f = Cost::template energy<0>(terms, n, a.family);
+            for (int r = 0; r < CL; ++r) cluster.map_shared_rank(scal, r)[0] = f;
+        }
+        csync();
+        return scal[0];
+    };
     // block-wide max (std::max semantics: NaN never replaces the running max)
     auto block_max = [&](double v) {
         for (int o = 16; o > 0; o >>= 1) {
@@ -101,36 +143,38 @@ __global__ void __launch_bounds__(512) nm_kernel(const NMArgs a) {
         __syncthreads();
         return r;
     };
-    // D[v] for one vertex against the current best (vertex id b)
+    auto col = [&](int v, int j) -> double& { return X[static_cast<size_t>(v) * n + c0 + j]; };
+    // D[v] over own columns against the current best (vertex id b)
     auto vertex_diameter = [&](int v, int b) {
         double d = 0;
-        for (int k = tid; k < n; k += B) {
-            const double t = fabs(X[static_cast<size_t>(v) * n + k] - X[static_cast<size_t>(b) * n + k]);
+        for (int j = tid; j < nc; j += B) {
+            const double t = fabs(col(v, j) - col(b, j));
             d = d < t ? t : d;
         }
         const double m = block_max(d);
         if (tid == 0) D[v] = m;
     };
-    auto set_vertex = [&](int v, const double* src) { // X[v] = src, Q[v] = src / n
-        for (int k = tid; k < n; k += B) {
-            X[static_cast<size_t>(v) * n + k] = src[k];
-            Q[static_cast<size_t>(v) * n + k] = src[k] / dn;
+    auto set_vertex = [&](int v, const double* src) { // X[v] = src, Q[v] = src / n (own columns)
+        for (int j = tid; j < nc; j += B) {
+            col(v, j) = src[j];
+            Qb[static_cast<size_t>(v) * qst + j] = src[j] / dn;
         }
     };
 
     // initial simplex (nelder_mead.cpp:50-59)
     for (int v = 0; v <= n; ++v) {
-        for (int k = tid; k < n; k += B) {
+        for (int j = tid; j < nc; j += B) {
+            const int k = c0 + j;
             double xk = a.x_start[k];
             if (v > 0 && k == v - 1) {
                 const double step = 0.05 * (a.upper[k] - a.lower[k]);
                 xk = (xk + step <= a.upper[k]) ? xk + step : xk - step;
             }
-            xr[k] = xk;
+            xr[j] = xk;
         }
         __syncthreads();
         set_vertex(v, xr);
-        const double fv = block_eval<Cost>(xr, n, a.family, terms, scal);
+        const double fv = eval(xr);
         if (tid == 0) {
             f_s[v] = fv;
             ord_s[v] = v;
@@ -138,7 +182,7 @@ __global__ void __launch_bounds__(512) nm_kernel(const NMArgs a) {
         ++evals;
         __syncthreads();
     }
-    for (int k = tid; k < n; k += B) P[k] = 0.0; // P[0] = the centroid's 0.0 fill
+    for (int j = tid; j < nc; j += B) Pb[j] = 0.0; // P[0] = the centroid's 0.0 fill
     if (tid == 0) {
         ist[0] = 0;  // valid centroid prefix length
         ist[1] = -1; // diameters stale
@@ -149,7 +193,8 @@ __global__ void __launch_bounds__(512) nm_kernel(const NMArgs a) {
     // vertex); if any two values are equivalent (equal or NaN) the order of
     // the tied vertices is what libstdc++'s introsort makes of the physical
     // order, so thread 0 runs that exact algorithm (parsa_stdsort.h).
-    int* saved = reinterpret_cast<int*>(terms) + 2 * (n + 1); // pre-sort physical order
+    int* rk = ist + 4;         // n+1 ints: ranks of the full sort
+    int* saved = rk + (n + 1); // n+1 ints: the pre-sort order
     auto equiv = [](double a, double b) { return !(a < b) && !(b < a); };
     auto exact_sort = [&]() {
         if (tid == 0) {
@@ -170,10 +215,10 @@ __global__ void __launch_bounds__(512) nm_kernel(const NMArgs a) {
                 const double fq = f_s[saved[q]];
                 r += (fq < fp) || (fq == fp && q < p);
             }
-            reinterpret_cast<int*>(terms)[p] = r;
+            rk[p] = r;
         }
         __syncthreads();
-        for (int p = tid; p <= n; p += B) ord_s[reinterpret_cast<int*>(terms)[p]] = saved[p];
+        for (int p = tid; p <= n; p += B) ord_s[rk[p]] = saved[p];
         __syncthreads();
         int tie = 0;
         for (int p = tid; p < n; p += B) tie |= equiv(f_s[ord_s[p]], f_s[ord_s[p + 1]]);
@@ -191,7 +236,7 @@ __global__ void __launch_bounds__(512) nm_kernel(const NMArgs a) {
     full_sort();
 
     // replace the worst vertex (physical position n) by the point in src
-    // (shared) with value fv, then std::sort
+    // (own columns) with value fv, then std::sort
     auto replace_worst = [&](const double* src, double fv) {
         const int w = ord_s[n];
         set_vertex(w, src);
@@ -234,12 +279,12 @@ __global__ void __launch_bounds__(512) nm_kernel(const NMArgs a) {
         // termination (nelder_mead.cpp:67-68; simplex_diameter :21-27)
         const int b0 = ord_s[0];
         if (ist[1] != b0) {
-            // all diameters against the best: one warp per vertex
+            // all diameters (own columns) against the best: one warp per vertex
             const int lane = tid & 31, warp = tid >> 5, nw = B >> 5;
             for (int v = warp; v <= n; v += nw) {
                 double d = 0;
-                for (int k = lane; k < n; k += 32) {
-                    const double t = fabs(X[static_cast<size_t>(v) * n + k] - X[static_cast<size_t>(b0) * n + k]);
+                for (int j = lane; j < nc; j += 32) {
+                    const double t = fabs(col(v, j) - col(b0, j));
                     d = d < t ? t : d;
                 }
                 for (int o = 16; o > 0; o >>= 1) {
@@ -254,39 +299,52 @@ __global__ void __launch_bounds__(512) nm_kernel(const NMArgs a) {
         }
         double dm = 0;
         for (int i = 1 + tid; i <= n; i += B) dm = dm < D[ord_s[i]] ? D[ord_s[i]] : dm;
-        const double dmax = block_max(dm);
+        dm = block_max(dm);
+        if (tid == 0)
+            for (int r = 0; r < CL; ++r) cluster.map_shared_rank(dslot, r)[rank] = dm;
+        csync();
+        double dmax = 0;
+        for (int r = 0; r < CL; ++r) dmax = dmax < dslot[r] ? dslot[r] : dmax;
         if (f_s[ord_s[n]] - f_s[ord_s[0]] <= a.f_tol || dmax <= a.x_tol) break;
 
-        // centroid of the n best (nelder_mead.cpp:70-73): re-add from the
-        // first position whose vertex changed
-        // (prefixes are stored every kNmCheckpoint positions: re-adding from
-        // the checkpoint at or below the first changed position costs a few
-        // adds, storing every prefix would cost an O(n^2) write stream)
+        // centroid of the n best (nelder_mead.cpp:70-73), own columns: re-add
+        // from the checkpoint at or below the first changed position (prefix
+        // sums are stored every kNmCheckpoint positions)
         const int vp = (ist[0] / kNmCheckpoint) * kNmCheckpoint;
-        for (int k = tid; k < n; k += B) {
-            double c = P[static_cast<size_t>(vp / kNmCheckpoint) * n + k];
-            for (int p = vp; p < n; ++p) {
-                c += Q[static_cast<size_t>(ord_s[p]) * n + k];
-                if ((p + 1) % kNmCheckpoint == 0) P[static_cast<size_t>((p + 1) / kNmCheckpoint) * n + k] = c;
+        for (int j = tid; j < nc; j += B) {
+            double c = Pb[static_cast<size_t>(vp / kNmCheckpoint) * qst + j];
+            // one checkpoint segment at a time: its (up to 16) quotients are
+            // loaded first, so the loads overlap each other instead of each
+            // add waiting for its own load
+            for (int p0 = vp; p0 < n; p0 += kNmCheckpoint) {
+                const int m = n - p0 < kNmCheckpoint ? n - p0 : kNmCheckpoint;
+                double q[kNmCheckpoint];
+#pragma unroll
+                for (int i = 0; i < kNmCheckpoint; ++i)
+                    if (i < m) q[i] = Qb[static_cast<size_t>(ord_s[p0 + i]) * qst + j];
+#pragma unroll
+                for (int i = 0; i < kNmCheckpoint; ++i)
+                    if (i < m) c += q[i];
+                if (m == kNmCheckpoint) Pb[static_cast<size_t>((p0 + m) / kNmCheckpoint) * qst + j] = c;
             }
-            cen[k] = c;
+            cen[j] = c;
         }
         __syncthreads();
         if (tid == 0) ist[0] = n;
         const int worst = ord_s[n];
         const double worst_f = f_s[worst];
-        for (int k = tid; k < n; k += B) {
-            const double wk = X[static_cast<size_t>(worst) * n + k];
-            xr[k] = clampd(cen[k] + a.reflect * (cen[k] - wk), a.lower[k], a.upper[k]);
+        for (int j = tid; j < nc; j += B) {
+            const int k = c0 + j;
+            xr[j] = clampd(cen[j] + a.reflect * (cen[j] - col(worst, j)), a.lower[k], a.upper[k]);
         }
         __syncthreads();
-        const double fr = block_eval<Cost>(xr, n, a.family, terms, scal);
+        const double fr = eval(xr);
         ++evals;
         if (fr < f_s[ord_s[0]]) {
-            for (int k = tid; k < n; k += B)
-                xe[k] = clampd(cen[k] + a.expand * (xr[k] - cen[k]), a.lower[k], a.upper[k]);
+            for (int j = tid; j < nc; j += B)
+                xe[j] = clampd(cen[j] + a.expand * (xr[j] - cen[j]), a.lower[c0 + j], a.upper[c0 + j]);
             __syncthreads();
-            const double fe = block_eval<Cost>(xe, n, a.family, terms, scal);
+            const double fe = eval(xe);
             ++evals;
             if (fe < fr) replace_worst(xe, fe);
             else replace_worst(xr, fr);
@@ -294,12 +352,12 @@ __global__ void __launch_bounds__(512) nm_kernel(const NMArgs a) {
             replace_worst(xr, fr);
         } else {
             const bool outside = fr < worst_f;
-            for (int k = tid; k < n; k += B) {
-                const double toward = outside ? xr[k] : X[static_cast<size_t>(worst) * n + k];
-                xc[k] = clampd(cen[k] + a.contract * (toward - cen[k]), a.lower[k], a.upper[k]);
+            for (int j = tid; j < nc; j += B) {
+                const double toward = outside ? xr[j] : col(worst, j);
+                xc[j] = clampd(cen[j] + a.contract * (toward - cen[j]), a.lower[c0 + j], a.upper[c0 + j]);
             }
             __syncthreads();
-            const double fc = block_eval<Cost>(xc, n, a.family, terms, scal);
+            const double fc = eval(xc);
             ++evals;
             if (fc < (outside ? fr : worst_f)) {
                 replace_worst(xc, fc);
@@ -308,14 +366,13 @@ __global__ void __launch_bounds__(512) nm_kernel(const NMArgs a) {
                 const int best = ord_s[0];
                 for (int i = 1; i <= n; ++i) {
                     const int v = ord_s[i];
-                    for (int k = tid; k < n; k += B) {
-                        const double x0 = X[static_cast<size_t>(best) * n + k];
-                        const double xv = X[static_cast<size_t>(v) * n + k];
-                        xr[k] = clampd(x0 + a.shrink * (xv - x0), a.lower[k], a.upper[k]);
+                    for (int j = tid; j < nc; j += B) {
+                        const double x0 = col(best, j);
+                        xr[j] = clampd(x0 + a.shrink * (col(v, j) - x0), a.lower[c0 + j], a.upper[c0 + j]);
                     }
                     __syncthreads();
                     set_vertex(v, xr);
-                    const double fv = block_eval<Cost>(xr, n, a.family, terms, scal);
+                    const double fv = eval(xr);
                     ++evals;
                     if (tid == 0) f_s[v] = fv;
                     __syncthreads();
@@ -326,20 +383,28 @@ __global__ void __launch_bounds__(512) nm_kernel(const NMArgs a) {
         __syncthreads();
     }
     const int b = ord_s[0];
-    for (int k = tid; k < n; k += B) a.x_best[k] = X[static_cast<size_t>(b) * n + k];
-    if (tid == 0) {
+    for (int j = tid; j < nc; j += B) a.x_best[c0 + j] = col(b, j);
+    if (rank == 0 && tid == 0) {
         a.out->f_best = f_s[b];
         a.out->iterations = iter;
         a.out->evaluations = evals;
     }
+    cluster.sync(); // no CTA may exit while others can still store into its shared memory
 }
 
-size_t nm_smem_bytes(int n) {
-    // cen, xr, xe, xc (4n) + terms (2n, also int scratch for 3(n+1) ids) +
-    // reduction/scalars (40) + values and diameters (2(n+1)) + order (n+1
-    // ints) + int scalars
-    return sizeof(double) * (6 * static_cast<size_t>(n) + 48 + 2 * (static_cast<size_t>(n) + 1)) +
-           sizeof(int) * (n + 1 + 4) + 64;
+// shared memory of one CTA of an NM cluster of `cl` CTAs; with q_smem the
+// CTA also keeps its columns' quotients Q ((n+1) x ceil(n/cl)) and centroid
+// checkpoints (n/16+1 rows) in shared memory
+size_t nm_smem_bytes(int n, int cl, bool q_smem) {
+    const size_t nc = (static_cast<size_t>(n) + cl - 1) / cl;
+    // doubles: terms (2n + 8), own-column cen/xr/xe/xc (4 nc), red/scal/dslot
+    // (56), f and D (2(n+1)); ints: order, ranks, saved order (3(n+1)) and
+    // scalars (4), padding (2)
+    size_t b = sizeof(double) * (2 * static_cast<size_t>(n) + 8 + 4 * nc + 56 + 2 * (static_cast<size_t>(n) + 1)) +
+               sizeof(int) * (3 * (static_cast<size_t>(n) + 1) + 6);
+    b = (b + 15) & ~size_t(15);
+    if (q_smem) b += sizeof(double) * nc * (static_cast<size_t>(n) + 1 + static_cast<size_t>(n) / kNmCheckpoint + 1);
+    return b + 64;
 }
 
 template <class Cost>
