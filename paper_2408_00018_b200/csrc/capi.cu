@@ -252,7 +252,7 @@ void plan_build(psa_plan* p, const psa_objective* f, const psa_engine_config* cf
     cudaDeviceProp prop;
     cuda_check(cudaGetDeviceProperties(&prop, dev), "cudaGetDeviceProperties");
     const size_t smem_cap = prop.sharedMemPerBlockOptin;
-    auto smem_of = [&](int B) { return engine == 1 ? p->ks.smem_v1(n, B) : p->ks.smem_v2(n, B); };
+    auto smem_of = [&](int B) { return engine == 1 ? p->ks.smem_v1(n, B, !uniform) : p->ks.smem_v2(n, B, !uniform); };
     int B = 128;
     while (B > 32 && smem_of(B) > smem_cap) B /= 2;
     // chain rows that do not fit in shared memory even at 32 threads per
@@ -263,11 +263,11 @@ void plan_build(psa_plan* p, const psa_objective* f, const psa_engine_config* cf
     p->hbm_rows = smem_of(B) > smem_cap || (force && force[0] == '1');
     if (p->hbm_rows) {
         B = 128;
-        if (p->ks.smem_g(n, B) > smem_cap)
+        if (p->ks.smem_g(n, B, !uniform) > smem_cap)
             fail(PSA_ERR_INVALID_ARGUMENT, "parsa_b200: dimension too large for the block-shared level state");
     }
     p->block = B;
-    p->smem = p->hbm_rows ? p->ks.smem_g(n, B) : smem_of(B);
+    p->smem = p->hbm_rows ? p->ks.smem_g(n, B, !uniform) : smem_of(B);
     const void* kern = engine == 1 ? (p->hbm_rows ? p->ks.v1g : p->ks.v1) : (p->hbm_rows ? p->ks.v2g : p->ks.v2);
     // binary32 separable families: two chains per thread (FADD2 fold) when
     // the pair rows fit (PSA_NO_PAIR=1 keeps one chain per thread)
@@ -283,8 +283,8 @@ void plan_build(psa_plan* p, const psa_objective* f, const psa_engine_config* cf
     const void* pair_kern = engine == 2 ? p->ks.v2p : p->ks.v1p;
     if (!p->hbm_rows && pair_kern && mode != "single" && !(no_pair && no_pair[0] == '1')) {
         int Bp = 128;
-        while (Bp > 32 && p->ks.smem_v2p(n, Bp) > smem_cap) Bp /= 2;
-        const size_t smem_p = p->ks.smem_v2p(n, Bp);
+        while (Bp > 32 && p->ks.smem_v2p(n, Bp, !uniform) > smem_cap) Bp /= 2;
+        const size_t smem_p = p->ks.smem_v2p(n, Bp, !uniform);
         if (smem_p <= smem_cap) {
             cuda_check(cudaFuncSetAttribute(pair_kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             static_cast<int>(smem_p)),
@@ -341,7 +341,8 @@ void plan_build(psa_plan* p, const psa_objective* f, const psa_engine_config* cf
         p->d_xrows.alloc((p->pair ? 2 : 1) * static_cast<size_t>(p->grid) * B * n);
     }
     const size_t threads = static_cast<size_t>(p->grid) * B;
-    if (p->hbm_rows) p->d_rows.alloc(threads * static_cast<size_t>(n) * p->ks.state_bytes);
+    // HBM rows: n*A values per thread, padded to whole 16-byte vectors
+    if (p->hbm_rows) p->d_rows.alloc(threads * ((static_cast<size_t>(n) * p->ks.state_bytes + 15) & ~size_t(15)));
 
     EngineArgs& a = p->args;
     a.n = n;

@@ -51,14 +51,18 @@ struct Vec16<double> {
 };
 
 // Large-n layout: when a thread's row does not fit in shared memory the rows
-// live in HBM, structure-of-arrays: value i of thread g at base[i*T + g]
-// (T = threads in the grid), so a warp's accesses to the same i are one
-// coalesced 128-byte (f32) / 256-byte (f64) transaction.
+// live in HBM as warp tiles of 16-byte vectors: value i of lane l of warp w
+// at base[((w * nv + i / W) * 32 + l) * W + i % W] (W = 4 f32 / 2 f64 values
+// per vector, nv vectors per row).  A warp's fold loads of one vector are a
+// single coalesced 512-byte LDG.128, and successive vectors are adjacent, so
+// the fold streams one contiguous tile (no TLB thrashing across a
+// thread-strided layout); p = the lane's first value, s = 32 * W.
 template <class R>
 struct StridedRow {
+    static constexpr int W = 16 / static_cast<int>(sizeof(R));
     R* p;
     size_t s;
-    PSA_DEV R& operator[](int i) const { return p[static_cast<size_t>(i) * s]; }
+    PSA_DEV R& operator[](int i) const { return p[static_cast<size_t>(i / W) * s + (i % W)]; }
 };
 
 template <class T>
@@ -160,16 +164,33 @@ struct SepCost {
             for (int e = mv * V::W; e < m; ++e) acc[e % A] = fold<R>(Fam::op(e % A), acc[e % A], row[e]);
         }
     }
-    // any row type with operator[] (the HBM layout): scalar loads, same order
+    // the HBM layout (StridedRow): 16-byte vector loads, issued 8 at a time
+    // so that 128 B per thread are in flight; same fold order
     template <class Row>
     PSA_DEV static R energy_any(const Row& row, int n, int) {
+        using V = Vec16<R>;
         R acc[A];
 #pragma unroll
         for (int a = 0; a < A; ++a) acc[a] = Fam::init(a, n);
-#pragma unroll 4
-        for (int k = 0; k < n; ++k) {
+        const int m = n * A;
+        const int full = m / V::W; // whole vectors
+        auto ld = [&](int q) { return *reinterpret_cast<const typename V::T*>(row.p + static_cast<size_t>(q) * row.s); };
+        auto fold_vec = [&](const typename V::T& v) {
 #pragma unroll
-            for (int a = 0; a < A; ++a) acc[a] = fold<R>(Fam::op(a), acc[a], row[k * A + a]);
+            for (int w = 0; w < V::W; ++w) acc[w % A] = fold<R>(Fam::op(w % A), acc[w % A], V::get(v, w));
+        };
+        int q = 0;
+        for (; q + 8 <= full; q += 8) {
+            typename V::T v[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) v[i] = ld(q + i);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) fold_vec(v[i]);
+        }
+        for (; q < full; ++q) fold_vec(ld(q));
+        if (m % V::W) { // (W is a multiple of A, so element e = full*W + w has array w % A)
+            const typename V::T v = ld(full);
+            for (int w = 0; w < m % V::W; ++w) acc[w % A] = fold<R>(Fam::op(w % A), acc[w % A], V::get(v, w));
         }
         return Fam::finish(acc, n);
     }

@@ -95,15 +95,15 @@ struct EngineKernels {
     const void* v1;
     const void* v2p; // chain pairs (binary32 separable families), or nullptr
     const void* v1p; // V1 with chain pairs, or nullptr
-    size_t (*smem_v2p)(int n, int B); // pair rows (the same for V1 pairs)
+    size_t (*smem_v2p)(int n, int B, bool box); // pair rows (the same for V1 pairs)
     const void* v2g; // HBM chain-state layout (large n)
     const void* v1g;
-    size_t (*smem_g)(int n, int B);
+    size_t (*smem_g)(int n, int B, bool box);
     size_t state_bytes; // sizeof(R) * A: bytes per coordinate of a chain row
     const void* eval;
     const void* sweep; // sweep_one: single caller-held chain (parsa::metropolis_sweep)
-    size_t (*smem_v2)(int n, int B);
-    size_t (*smem_v1)(int n, int B);
+    size_t (*smem_v2)(int n, int B, bool box);
+    size_t (*smem_v1)(int n, int B, bool box);
     size_t (*smem_eval)(int n, int B);
 };
 

@@ -60,7 +60,7 @@ struct Smem {
 };
 
 template <class R, int A>
-size_t engine_smem_bytes(int n, int B, bool rows_in_smem, bool pair = false) {
+size_t engine_smem_bytes(int n, int B, bool box, bool rows_in_smem, bool pair = false) {
     size_t off = 0;
     auto take = [&](size_t bytes) {
         off = (off + 15) & ~size_t(15);
@@ -69,8 +69,8 @@ size_t engine_smem_bytes(int n, int B, bool rows_in_smem, bool pair = false) {
     if (rows_in_smem) take(sizeof(R) * size_t(row_stride<R>(pair ? 2 * n : n, A)) * B); // per-thread state rows
     take(sizeof(double) * n);            // x*
     take(sizeof(R) * size_t(n) * A);     // V*
-    take(sizeof(double) * n);            // lower
-    take(sizeof(double) * n);            // width
+    if (box) take(sizeof(double) * n);   // lower (only for a non-uniform box)
+    if (box) take(sizeof(double) * n);   // width
     take(sizeof(Cand) * 34);             // reduction scratch
     take(64);                            // scalars
     return off;
@@ -122,8 +122,12 @@ struct RowSel<R, false> {
 template <class R>
 struct RowSel<R, true> {
     using T = StridedRow<R>;
-    static __device__ T make(R*, int, const EngineArgs& a, size_t gtid) {
-        return T{static_cast<R*>(a.rows) + gtid, a.threads};
+    // S = n*A values per row; a warp's 32 rows form one contiguous tile of
+    // nv = ceil(S/W) vectors x 32 lanes, so a fold walks its tile
+    // sequentially (512 B per vector step: coalesced, and page/TLB-local)
+    static __device__ T make(R*, int S, const EngineArgs& a, size_t gtid) {
+        const size_t nv = (static_cast<size_t>(S) + T::W - 1) / T::W;
+        return T{static_cast<R*>(a.rows) + ((gtid / 32) * nv * 32 + (gtid % 32)) * T::W, 32 * T::W};
     }
 };
 
@@ -295,8 +299,8 @@ __device__ __forceinline__ void v2_body(const EngineArgs& a) {
     R* V = G ? nullptr : sm.take<R>(static_cast<size_t>(S) * B);
     double* xs = sm.take<double>(n);
     R* vs = sm.take<R>(static_cast<size_t>(n) * A);
-    double* lower = sm.take<double>(n);
-    double* width = sm.take<double>(n);
+    double* lower = a.uniform_box ? nullptr : sm.take<double>(n);
+    double* width = a.uniform_box ? nullptr : sm.take<double>(n);
     Cand* scratch = sm.take<Cand>(34);
     SharedScalars* sh = sm.take<SharedScalars>(1);
 
@@ -509,8 +513,8 @@ __global__ void __launch_bounds__(256) v1_kernel(const EngineArgs a) {
     R* V = G ? nullptr : sm.take<R>(static_cast<size_t>(S) * B);
     double* xs = sm.take<double>(n);
     R* vs = sm.take<R>(static_cast<size_t>(n) * A);
-    double* lower = sm.take<double>(n);
-    double* width = sm.take<double>(n);
+    double* lower = a.uniform_box ? nullptr : sm.take<double>(n);
+    double* width = a.uniform_box ? nullptr : sm.take<double>(n);
     Cand* scratch = sm.take<Cand>(34);
     SharedScalars* sh = sm.take<SharedScalars>(1);
 
@@ -621,8 +625,8 @@ __global__ void __launch_bounds__(128, 3) v1_pair_kernel(const EngineArgs a) {
     float* V = sm.take<float>(static_cast<size_t>(S) * B);
     double* xs = sm.take<double>(n);
     float* vs = sm.take<float>(static_cast<size_t>(n) * A);
-    double* lower = sm.take<double>(n);
-    double* width = sm.take<double>(n);
+    double* lower = a.uniform_box ? nullptr : sm.take<double>(n);
+    double* width = a.uniform_box ? nullptr : sm.take<double>(n);
     Cand* scratch = sm.take<Cand>(34);
     SharedScalars* sh = sm.take<SharedScalars>(1);
 
@@ -823,21 +827,21 @@ struct KernelSet {
         k.v1 = reinterpret_cast<const void*>(&v1_kernel<R, Cost, NT, false>);
         k.v2g = reinterpret_cast<const void*>(&v2_kernel<R, Cost, 0, true>);
         k.v1g = reinterpret_cast<const void*>(&v1_kernel<R, Cost, 0, true>);
-        k.smem_g = [](int n, int B) { return engine_smem_bytes<R, Cost::A>(n, B, false); };
+        k.smem_g = [](int n, int B, bool box) { return engine_smem_bytes<R, Cost::A>(n, B, box, false); };
         k.state_bytes = sizeof(R) * Cost::A;
         k.eval = reinterpret_cast<const void*>(&probe_evaluate<R, Cost>);
         k.sweep = reinterpret_cast<const void*>(&sweep_one<R, Cost>);
-        k.smem_v2 = [](int n, int B) { return engine_smem_bytes<R, Cost::A>(n, B, true); };
+        k.smem_v2 = [](int n, int B, bool box) { return engine_smem_bytes<R, Cost::A>(n, B, box, true); };
         if constexpr (PairOf<Cost>::value) {
             k.v1p = reinterpret_cast<const void*>(&v1_pair_kernel<R, Cost, NT>);
             k.v2p = reinterpret_cast<const void*>(&v2_pair_kernel<R, Cost, NT>);
-            k.smem_v2p = [](int n, int B) { return engine_smem_bytes<R, Cost::A>(n, B, true, true); };
+            k.smem_v2p = [](int n, int B, bool box) { return engine_smem_bytes<R, Cost::A>(n, B, box, true, true); };
         } else {
             k.v1p = nullptr;
             k.v2p = nullptr;
             k.smem_v2p = nullptr;
         }
-        k.smem_v1 = [](int n, int B) { return engine_smem_bytes<R, Cost::A>(n, B, true); };
+        k.smem_v1 = [](int n, int B, bool box) { return engine_smem_bytes<R, Cost::A>(n, B, box, true); };
         k.smem_eval = [](int n, int B) { return sizeof(R) * size_t(row_stride<R>(n, Cost::A)) * B; };
         return k;
     }
