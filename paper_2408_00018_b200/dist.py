@@ -1,6 +1,10 @@
-"""Multi-GPU synchronous SA: one process per GPU, chains sharded by global
-index, the per-level minloc exchanged inside the persistent kernel through
-peer-mapped mailboxes (engine.cu: exchange_level).
+"""Multi-GPU SA: one process per GPU, chains sharded by global index.
+
+Synchronous engine (V2): the per-level minloc is exchanged inside the
+persistent kernel through peer-mapped mailboxes (exchange_level).
+Asynchronous engine (V1): the chains never interact, so each GPU runs its
+shard to the end and the ranks combine one small record each (end-state
+winner, per-level trace minima, counts) — run_asynchronous_sharded.
 
 torch.distributed is only the control plane here: it exchanges the CUDA IPC
 handles of the mailboxes once (all_gather_object) and provides barriers; no
@@ -14,7 +18,7 @@ from __future__ import annotations
 import math
 from typing import Sequence
 
-from .api import Candidate, EngineConfig, ObjectiveFunction, Plan
+from .api import Candidate, EngineConfig, ObjectiveFunction, Plan, RunResult, TracePoint
 
 
 def shard_range(n_chains: int, rank: int, world: int) -> tuple[int, int]:
@@ -56,3 +60,47 @@ def make_sharded_plan(f: ObjectiveFunction, cfg: EngineConfig, group=None, max_b
         plan.set_peers(peers)
         dist.barrier(group)
     return plan
+
+
+def combine_async_shards(results: Sequence[RunResult]) -> RunResult:
+    """Merge the shard results of one asynchronous run (engines.cpp:66-123)
+    into the single-GPU result, bit for bit: the end-state winner by the
+    engines' selection order (select_record), the per-level trace as the
+    minimum over shards of each shard's minimum (the device trace skips NaN
+    chains and reports +inf for a level without a finite value, so a plain
+    min over shards is the min over all chains), evaluations and draws as
+    sums; cumulative_evals already count the global chain range."""
+    if not results:
+        raise ValueError("combine_async_shards: no shard results")
+    w = select_record([Candidate(r.best_x, r.best_f, r.winning_chain) for r in results])
+    win = results[w]
+    levels = len(win.trace)
+    trace = []
+    for l in range(levels):
+        vals = [r.trace[l].best_f for r in results]
+        trace.append(TracePoint(win.trace[l].level, win.trace[l].cumulative_evals, min(vals)))
+    return RunResult(best_x=list(win.best_x), best_f=win.best_f,
+                     evaluations=sum(r.evaluations for r in results),
+                     wall_time_s=max(r.wall_time_s for r in results), trace=trace,
+                     winning_chain=win.winning_chain, rng_draws=sum(r.rng_draws for r in results))
+
+
+def run_asynchronous_sharded(f: ObjectiveFunction, cfg: EngineConfig, group=None, stream: int = 0) -> RunResult:
+    """V1 over the ranks of `group` (one GPU each): this rank's shard on its
+    device, then one all_gather of the shard results; every rank returns the
+    identical, single-GPU-equal RunResult."""
+    import time
+
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    begin, end = shard_range(cfg.n_chains, rank, world)
+    t0 = time.perf_counter()
+    with Plan(f, cfg, engine=1, chain_begin=begin, chain_end=end) as plan:
+        plan.launch(stream)
+        mine = plan.fetch(stream)
+    mine.wall_time_s = time.perf_counter() - t0
+    shards = [None] * world
+    dist.all_gather_object(shards, mine, group=group)
+    return combine_async_shards(shards)

@@ -81,3 +81,17 @@ def test_gloo_world2_exchange(world):
     for rank, sp, hs, picks in out:
         assert sp == spans and hs == list(range(world))
         assert len(set(picks)) == 1  # same winner everywhere
+
+
+def test_combine_async_shards_semantics():
+    from paper_2408_00018_b200.api import RunResult, TracePoint
+    from paper_2408_00018_b200.dist import combine_async_shards
+    inf = float("inf")
+    a = RunResult(best_x=[1.0], best_f=-2.0, evaluations=10, trace=[TracePoint(0, 30, -1.0), TracePoint(1, 60, -2.0)],
+                  winning_chain=4, rng_draws=27)
+    b = RunResult(best_x=[2.0], best_f=-2.0, evaluations=10, trace=[TracePoint(0, 30, inf), TracePoint(1, 60, -3.0)],
+                  winning_chain=1, rng_draws=27)
+    c = combine_async_shards([a, b])
+    assert c.winning_chain == 1 and c.best_x == [2.0]  # tie -> smaller global chain
+    assert [t.best_f for t in c.trace] == [-1.0, -3.0]
+    assert c.evaluations == 20 and c.rng_draws == 54
