@@ -493,9 +493,10 @@ PSA_DEV void pair_energy(const float* row, int n_rt, float& eA, float& eB) {
 // sweep() of sa_core.cpp:61-79 for two chains at once.  Each chain's draws,
 // proposals, energies and decisions are exactly those of sweep(); only the
 // fold is shared (FADD2).  Accept bits go to maskA/maskB[w * mask_stride].
-// (V1 passes no masks and the chains' double-precision points xa/xb, which
-// accepted moves update, x[k * xs].)
-template <template <class> class F, int NT>
+// (V1, kX = true: no masks; the chains' double-precision points xa/xb are
+// updated by accepted moves, x[k * xs].)  Trials run in words of 32, one
+// accept-mask word each.
+template <template <class> class F, int NT, bool kX = false>
 PSA_DEV void sweep_pair(float* row, int n_rt, float& EA, float& EB, double temperature, uint32_t cA,
                         uint32_t cB, uint32_t level, uint32_t ctr, int N, const Box& box, const PhiloxKeys& keys,
                         uint32_t* maskA, uint32_t* maskB, size_t mask_stride, double* xa = nullptr,
@@ -508,7 +509,6 @@ PSA_DEV void sweep_pair(float* row, int n_rt, float& EA, float& EB, double tempe
     const PhiloxChain pa = philox_chain(cA, level, keys);
     const PhiloxChain pb = philox_chain(cB, level, keys);
     const double idx_scale = static_cast<double>(n) * 0x1.0p-53;
-    uint32_t wordA = 0, wordB = 0;
     int dA, dB;
     double xA, xB;
     float tA[A], tB[A];
@@ -522,7 +522,10 @@ PSA_DEV void sweep_pair(float* row, int n_rt, float& EA, float& EB, double tempe
         Cost::cache(static_cast<float>(xA), dA, n, tA);
         Cost::cache(static_cast<float>(xB), dB, n, tB);
     }
-    for (int j = 0; j < N; ++j) {
+    for (int j0 = 0; j0 < N; j0 += 32) {
+    const int jn = N - j0 < 32 ? N - j0 : 32;
+    uint32_t wordA = 0, wordB = 0;
+    for (int j = 0; j < jn; ++j) {
         float oA[A], oB[A];
 #pragma unroll
         for (int a = 0; a < A; ++a) {
@@ -570,9 +573,9 @@ PSA_DEV void sweep_pair(float* row, int n_rt, float& EA, float& EB, double tempe
         ctr += 3;
         EA = rA ? trA : EA;
         EB = rB ? trB : EB;
-        wordA |= static_cast<uint32_t>(rA) << (j & 31);
-        wordB |= static_cast<uint32_t>(rB) << (j & 31);
-        if (xa) {
+        wordA |= static_cast<uint32_t>(rA) << j;
+        wordB |= static_cast<uint32_t>(rB) << j;
+        if constexpr (kX) {
             if (rA) xa[static_cast<size_t>(dA) * xs] = xA;
             if (rB) xb[static_cast<size_t>(dB) * xs] = xB;
         }
@@ -580,14 +583,6 @@ PSA_DEV void sweep_pair(float* row, int n_rt, float& EA, float& EB, double tempe
         for (int a = 0; a < A; ++a) {
             if (!rA) row[2 * (dA * A + a)] = oA[a];
             if (!rB) row[2 * (dB * A + a) + 1] = oB[a];
-        }
-        if ((j & 31) == 31 || j == N - 1) {
-            if (maskA) {
-                maskA[static_cast<size_t>(j >> 5) * mask_stride] = wordA;
-                maskB[static_cast<size_t>(j >> 5) * mask_stride] = wordB;
-            }
-            wordA = 0;
-            wordB = 0;
         }
         dA = nA;
         dB = nB;
@@ -598,6 +593,11 @@ PSA_DEV void sweep_pair(float* row, int n_rt, float& EA, float& EB, double tempe
             tA[a] = uA[a];
             tB[a] = uB[a];
         }
+    }
+    if constexpr (!kX) {
+        maskA[static_cast<size_t>(j0 >> 5) * mask_stride] = wordA;
+        maskB[static_cast<size_t>(j0 >> 5) * mask_stride] = wordB;
+    }
     }
 }
 

@@ -278,7 +278,7 @@ struct PairOf<SepCost<float, F>> {
     static __device__ void run_x(float* row, int n, float& eA, float& eB, double T, uint32_t cA, uint32_t cB,
                                  uint32_t ctr, int N, const Box& box, const PhiloxKeys& keys, double* xa, double* xb,
                                  size_t xs) {
-        sweep_pair<F, NT>(row, n, eA, eB, T, cA, cB, 0u, ctr, N, box, keys, nullptr, nullptr, 0, xa, xb, xs);
+        sweep_pair<F, NT, true>(row, n, eA, eB, T, cA, cB, 0u, ctr, N, box, keys, nullptr, nullptr, 0, xa, xb, xs);
     }
     template <int NT>
     static __device__ void energy(const float* row, int n, float& eA, float& eB) {
