@@ -340,9 +340,9 @@ PSA_DEV R sweep(Row row, int n_rt, int family, R E, double temperature, uint32_t
     const float k2 = static_cast<float>(1.4426950408889634 / temperature); // log2(e) / T
     const PhiloxChain pc = philox_chain(chain, level, keys);
     const double idx_scale = static_cast<double>(n) * 0x1.0p-53; // u*n == m*(n*2^-53) exactly
-    uint32_t word = 0;
     // trial 0's proposal; thereafter trial j+1's proposal (coordinate, value,
-    // new cached term) is built while trial j's fold runs
+    // new cached term) is built while trial j's fold runs.  Trials run in
+    // words of 32 (one accept-mask word each).
     int d;
     double xnew;
     R tn[A];
@@ -353,7 +353,10 @@ PSA_DEV R sweep(Row row, int n_rt, int family, R E, double temperature, uint32_t
         xnew = box.point(d, bits_to_uniform(m2));
         Cost::cache(static_cast<R>(xnew), d, n, tn);
     }
-    for (int j = 0; j < N; ++j) {
+    for (int j0 = 0; j0 < N; j0 += 32) {
+    const int jn = N - j0 < 32 ? N - j0 : 32;
+    uint32_t word = 0;
+    for (int j = 0; j < jn; ++j) {
         R to[A];
 #pragma unroll
         for (int a = 0; a < A; ++a) {
@@ -393,20 +396,18 @@ PSA_DEV R sweep(Row row, int n_rt, int family, R E, double temperature, uint32_t
         ctr += 3;
         if (acc) {
             E = trial;
-            word |= 1u << (j & 31);
+            word |= 1u << j;
             if (x) x[static_cast<size_t>(d) * x_stride] = xnew;
         } else {
 #pragma unroll
             for (int a = 0; a < A; ++a) row[d * A + a] = to[a];
         }
-        if ((j & 31) == 31 || j == N - 1) {
-            if (mask) mask[static_cast<size_t>(j >> 5) * mask_stride] = word;
-            word = 0;
-        }
         d = dn;
         xnew = xn;
 #pragma unroll
         for (int a = 0; a < A; ++a) tn[a] = tnn[a];
+    }
+    if (mask) mask[static_cast<size_t>(j0 >> 5) * mask_stride] = word;
     }
     st.evals += static_cast<uint64_t>(N);
     st.draws += 3ull * static_cast<uint64_t>(N);
