@@ -14,6 +14,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <sstream>
 #include <string>
 #include <vector>
@@ -135,18 +136,42 @@ std::vector<double> resolve_start(const psa_objective* f, const psa_engine_confi
     return s;
 }
 
+// sm_100 devices visible to this process; queried once (cudaGetDeviceProperties
+// costs milliseconds per device and every engine call checks for a device)
 int device_count_sm100() {
-    int n = 0;
-    if (cudaGetDeviceCount(&n) != cudaSuccess) {
-        cudaGetLastError();
-        return 0;
-    }
-    int ok = 0;
-    for (int d = 0; d < n; ++d) {
-        cudaDeviceProp p;
-        if (cudaGetDeviceProperties(&p, d) == cudaSuccess && p.major == 10) ++ok;
-    }
-    return ok;
+    static const int count = [] {
+        int n = 0;
+        if (cudaGetDeviceCount(&n) != cudaSuccess) {
+            cudaGetLastError();
+            return 0;
+        }
+        int ok = 0;
+        for (int d = 0; d < n; ++d) {
+            int major = 0;
+            if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, d) == cudaSuccess && major == 10) ++ok;
+        }
+        return ok;
+    }();
+    return count;
+}
+
+// per-device launch limits, cached (the same device query on every plan)
+struct DeviceLimits {
+    int sms = 0;
+    size_t smem_optin = 0;
+};
+const DeviceLimits& device_limits(int dev) {
+    static DeviceLimits cache[64];
+    static std::once_flag once[64];
+    const int d = dev < 0 || dev >= 64 ? 0 : dev;
+    std::call_once(once[d], [&] {
+        int v = 0;
+        cuda_check(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d), "cudaDeviceGetAttribute");
+        cache[d].sms = v;
+        cuda_check(cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, d), "cudaDeviceGetAttribute");
+        cache[d].smem_optin = static_cast<size_t>(v);
+    });
+    return cache[d];
 }
 
 void require_device() {
@@ -249,9 +274,8 @@ void plan_build(psa_plan* p, const psa_objective* f, const psa_engine_config* cf
     // block size: the largest of 128/64/32 whose state fits in shared memory
     int dev = 0;
     cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
-    cudaDeviceProp prop;
-    cuda_check(cudaGetDeviceProperties(&prop, dev), "cudaGetDeviceProperties");
-    const size_t smem_cap = prop.sharedMemPerBlockOptin;
+    const DeviceLimits& lim = device_limits(dev);
+    const size_t smem_cap = lim.smem_optin;
     auto smem_of = [&](int B) { return engine == 1 ? p->ks.smem_v1(n, B, !uniform) : p->ks.smem_v2(n, B, !uniform); };
     int B = 128;
     while (B > 32 && smem_of(B) > smem_cap) B /= 2;
@@ -291,7 +315,7 @@ void plan_build(psa_plan* p, const psa_objective* f, const psa_engine_config* cf
                        "cudaFuncSetAttribute");
             int per_sm_p = 0;
             cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_p, pair_kern, Bp, smem_p), "occupancy");
-            const long long pair_threads = static_cast<long long>(per_sm_p) * Bp * prop.multiProcessorCount;
+            const long long pair_threads = static_cast<long long>(per_sm_p) * Bp * lim.sms;
             const long long pairs = (static_cast<long long>(p->chains_local) + 1) / 2;
             const bool worth = per_sm_p * Bp >= 256 && pairs >= pair_threads;
             if (worth || mode == "pair") {
@@ -311,7 +335,7 @@ void plan_build(psa_plan* p, const psa_objective* f, const psa_engine_config* cf
     if (per_sm < 1) fail(PSA_ERR_CUDA, "parsa_b200: engine kernel cannot be resident");
     const long long units = p->pair ? (static_cast<long long>(p->chains_local) + 1) / 2 : p->chains_local;
     const long long need = (units + B - 1) / B;
-    p->grid = static_cast<int>(std::min<long long>(need, static_cast<long long>(per_sm) * prop.multiProcessorCount));
+    p->grid = static_cast<int>(std::min<long long>(need, static_cast<long long>(per_sm) * lim.sms));
     if (p->max_blocks > 0) p->grid = std::min(p->grid, p->max_blocks);
 
     // device buffers
