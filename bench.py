@@ -55,6 +55,7 @@ def parse():
     ap.add_argument("--chains", type=int, default=CHAINS_PER_GPU, help="chains per GPU")
     ap.add_argument("--tmin", type=float, default=SCHEDULE[1], help="override Tmin (shorter ladder)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-companion", action="store_true", help="skip the other-precision companion run")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     return ap.parse_args()
 
@@ -264,6 +265,8 @@ def main():
 
     # end-to-end through the public C-ABI with host buffers (per rank: its shard)
     e2e_ms = []
+    e2e_sampler = ClockSampler(local)
+    e2e_sampler.start()
     for i in range(max(1, min(args.steps, 3)) + 1):
         barrier()
         t0 = time.perf_counter()
@@ -277,6 +280,7 @@ def main():
         dt = (time.perf_counter() - t0) * 1e3
         if i > 0:  # first call pays the one-time module/context setup
             e2e_ms.append(dt)
+    e2e_clocks = e2e_sampler.stop()
     te = torch.tensor([statistics.mean(e2e_ms)], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
@@ -329,7 +333,7 @@ def main():
                    "parallelism": f"chains sharded over {world} GPU(s), per-level minloc over NVLink peer mailboxes"
                    if world > 1 else "1 GPU"},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "api": "psa_run_synchronous (C-ABI, host buffers)"},
+                "api": "psa_run_synchronous (C-ABI, host buffers)", "ms_per_call": e2e_ms, "clocks": e2e_clocks},
         "gpu_launches": args.steps * plan.launches_per_run,
         "roofline": {"bound": "smem", "achieved": achieved_bw / 1e9, "peak": smem_peak / 1e9, "unit": "GB/s",
                      "frac": achieved_bw / smem_peak, "traffic": traffic,
@@ -345,6 +349,29 @@ def main():
         "clocks": clocks,
         "result": {"best_f": res.best_f, "winning_chain": res.winning_chain, "evaluations": res.evaluations},
     }
+    # companion measurement in the other precision (the reference engines
+    # default to double precision, the paper's GPU code to single): same
+    # workload and timing method, one timed step after one warm-up
+    if world == 1 and not args.no_companion:
+        other = psa.Precision.f64 if prec == psa.Precision.f32 else psa.Precision.f32
+        cfg2 = psa.EngineConfig(n_chains=total_chains, schedule=sched, precision=other, seed=0)
+        with psa.Plan(f, cfg2, engine=2) as p2:
+            p2.launch(sh)
+            p2.fetch(sh)
+            flush.fill_(1.0)
+            barrier()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            p2.launch(sh)
+            e1.record(stream)
+            barrier()
+            ms2 = e0.elapsed_time(e1)
+            r2 = p2.fetch(sh)
+            line["companion"] = {"dtype": "f64" if other == psa.Precision.f64 else "f32",
+                                 "value": evals_per_step / (ms2 / 1e3), "unit": UNIT, "ms_per_step": ms2,
+                                 "kernel": p2.description, "best_f": r2.best_f,
+                                 "note": "same workload in the other precision; not the headline"}
     if rank == 0 and not args.no_cpu_baseline:
         try:
             rate, sample, threads, *_ = reference_sample(1 if args.precision == "f32" else 0, args.cpu_seconds)

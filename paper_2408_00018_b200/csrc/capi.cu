@@ -179,6 +179,25 @@ void require_device() {
         fail(PSA_ERR_NO_DEVICE, "parsa_b200: no sm_100 CUDA device available (there is no CPU fallback)");
 }
 
+// Device buffers come from the device's stream-ordered memory pool, which
+// keeps freed memory for reuse (release threshold: unlimited), so repeated
+// engine calls do not pay cudaMalloc/cudaFree (and cudaFree's implicit device
+// synchronisation).  Allocation and release are ordered on the legacy
+// stream; every user of a buffer has completed before it is released (the
+// engine entry points synchronise their stream, psa_plan_destroy the device).
+void retain_pool_memory() {
+    static std::once_flag once;
+    std::call_once(once, [] {
+        int dev = 0;
+        cudaMemPool_t pool;
+        if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t keep = ~0ull;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+        cudaGetLastError();
+    });
+}
+
 template <class T>
 struct DevBuf {
     T* p = nullptr;
@@ -186,10 +205,14 @@ struct DevBuf {
     void alloc(size_t count) {
         free();
         n = count;
-        if (count) cuda_check(cudaMalloc(&p, sizeof(T) * count), "cudaMalloc");
+        if (count) {
+            retain_pool_memory();
+            cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&p), sizeof(T) * count, 0), "cudaMallocAsync");
+            cuda_check(cudaStreamSynchronize(0), "cudaMallocAsync");
+        }
     }
     void free() {
-        if (p) cudaFree(p);
+        if (p) cudaFreeAsync(p, 0);
         p = nullptr;
         n = 0;
     }
@@ -817,6 +840,7 @@ psa_status psa_plan_level_detail(const psa_plan* p, int32_t* winners, double* wi
 }
 
 psa_status psa_plan_destroy(psa_plan* p) {
+    cudaDeviceSynchronize(); // its buffers return to the pool only after every use
     delete p;
     return PSA_OK;
 }

@@ -3,6 +3,6 @@
 cd "$(dirname "$0")/.."
 for d in gpu_variants/*/; do
   n=$(basename $d)
-  v=$(PSA_LIB_PATH=$PWD/$d/libparsa_b200.so timeout 300 python bench.py --tmin 500 --no-cpu-baseline --steps 3 --warmup 3 "$@" 2>gpurun_out/variant_$n.err | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('%.4e'%d['value'])")
+  v=$(PSA_LIB_PATH=$PWD/$d/libparsa_b200.so timeout 300 python bench.py --tmin 500 --no-cpu-baseline --no-companion --steps 3 --warmup 3 "$@" 2>gpurun_out/variant_$n.err | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('%.4e'%d['value'])")
   echo "$n $v"
 done
