@@ -340,18 +340,28 @@ PSA_DEV R sweep(Row row, int n_rt, int family, R E, double temperature, uint32_t
     const float k2 = static_cast<float>(1.4426950408889634 / temperature); // log2(e) / T
     const PhiloxChain pc = philox_chain(chain, level, keys);
     const double idx_scale = static_cast<double>(n) * 0x1.0p-53; // u*n == m*(n*2^-53) exactly
-    // trial 0's proposal; thereafter trial j+1's proposal (coordinate, value,
-    // new cached term) is built while trial j's fold runs.  Trials run in
+    // Two-stage software pipeline over the trials (the streams are counter-
+    // based, so every draw is known in advance).  While trial j's fold and
+    // decision run, the same iteration builds trial j+1's new term from
+    // draws made one iteration earlier and makes trial j+2's three draws:
+    // three independent dependency chains the scheduler interleaves, instead
+    // of one long Philox -> index -> sinf chain per trial.  Trials run in
     // words of 32 (one accept-mask word each).
-    int d;
+    int d;          // trial j: coordinate, value, new cached term, acceptance draw
     double xnew;
     R tn[A];
+    uint64_t m3;
+    uint64_t q1, q2, q3; // trial j+1's draws
     {
         const uint64_t m1 = draw_bits53_fast(ctr, pc, keys);
         const uint64_t m2 = draw_bits53_fast(ctr + 1, pc, keys);
+        m3 = draw_bits53_fast(ctr + 2, pc, keys);
         d = min(static_cast<int>(static_cast<double>(m1) * idx_scale), n - 1);
         xnew = box.point(d, bits_to_uniform(m2));
         Cost::cache(static_cast<R>(xnew), d, n, tn);
+        q1 = draw_bits53_fast(ctr + 3, pc, keys);
+        q2 = draw_bits53_fast(ctr + 4, pc, keys);
+        q3 = draw_bits53_fast(ctr + 5, pc, keys);
     }
     for (int j0 = 0; j0 < N; j0 += 32) {
     const int jn = N - j0 < 32 ? N - j0 : 32;
@@ -363,20 +373,19 @@ PSA_DEV R sweep(Row row, int n_rt, int family, R E, double temperature, uint32_t
             to[a] = row[d * A + a];
             row[d * A + a] = tn[a];
         }
-        // independent of this trial's outcome: its acceptance draw and the
-        // next proposal (the streams are counter-based)
-        const uint64_t m3 = draw_bits53_fast(ctr + 2, pc, keys);
-        const uint64_t m1 = draw_bits53_fast(ctr + 3, pc, keys);
-        const uint64_t m2 = draw_bits53_fast(ctr + 4, pc, keys);
-        const int dn = min(static_cast<int>(static_cast<double>(m1) * idx_scale), n - 1);
-        const double xn = box.point(dn, bits_to_uniform(m2));
+        // trial j+1's proposal from its draws, trial j+2's draws
+        const int dn = min(static_cast<int>(static_cast<double>(q1) * idx_scale), n - 1);
+        const double xn = box.point(dn, bits_to_uniform(q2));
         R tnn[A];
         bool ok;
         Cost::cache_common(static_cast<R>(xn), dn, n, tnn, ok);
+        const uint64_t r1 = draw_bits53_fast(ctr + 6, pc, keys);
+        const uint64_t r2 = draw_bits53_fast(ctr + 7, pc, keys);
+        const uint64_t r3 = draw_bits53_fast(ctr + 8, pc, keys);
 #ifndef PSA_NO_PIN
         // materialise them here so the scheduler interleaves them into the
         // fold's FADD latency chain (left alone, the compiler sinks them)
-        asm volatile("" ::"l"(m3), "r"(dn));
+        asm volatile("" ::"l"(r1), "l"(r2), "l"(r3), "r"(dn));
 #pragma unroll
         for (int a = 0; a < A; ++a) {
             if constexpr (sizeof(R) == 4) asm volatile("" ::"f"(tnn[a]));
@@ -404,6 +413,10 @@ PSA_DEV R sweep(Row row, int n_rt, int family, R E, double temperature, uint32_t
         }
         d = dn;
         xnew = xn;
+        m3 = q3;
+        q1 = r1;
+        q2 = r2;
+        q3 = r3;
 #pragma unroll
         for (int a = 0; a < A; ++a) tn[a] = tnn[a];
     }
