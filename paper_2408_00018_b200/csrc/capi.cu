@@ -234,6 +234,7 @@ struct psa_plan {
     EngineArgs args{};
     bool hbm_rows = false;        // chain rows in HBM (large n) instead of shared memory
     bool pair = false;            // two chains per thread (v2_pair_kernel)
+    bool pc = false;              // producer/consumer blocks (v2_pc_kernel)
     size_t mask_stride = 0;
     const void* kernel = nullptr; // the engine kernel this plan launches
     DevBuf<double> d_lower, d_width, d_start, d_temps, d_trace, d_bestx, d_xbest, d_winner_f, d_xrows;
@@ -327,8 +328,20 @@ void plan_build(psa_plan* p, const psa_objective* f, const psa_engine_config* cf
     // the pair kernel still keeps >= 8 warps per SM resident and there are
     // enough pairs to fill them (small chain counts or large n keep one chain
     // per thread; PSA_V2_MODE=pair forces pairs whenever the rows fit).
+    // Few chains (fewer than 8 warps per SM of one chain per thread): each
+    // chain's level is a latency-bound dependency chain, so producer warps
+    // take the proposals off its critical path (v2_pc_kernel).
+    const bool few = static_cast<long long>(p->chains_local) < 256ll * lim.sms;
+    if (engine == 2 && !p->hbm_rows && p->ks.v2pc && (mode == "pc" || (mode.empty() && few)) &&
+        p->ks.smem_v2pc(n, 128, !uniform) <= smem_cap) {
+        p->pc = true;
+        p->block = B = 128;
+        p->smem = p->ks.smem_v2pc(n, 128, !uniform);
+        kern = p->ks.v2pc;
+    }
     const void* pair_kern = engine == 2 ? p->ks.v2p : p->ks.v1p;
-    if (!p->hbm_rows && pair_kern && mode != "single" && !(no_pair && no_pair[0] == '1')) {
+    if (!p->pc && !p->hbm_rows && pair_kern && mode != "single" && mode != "pc" &&
+        !(no_pair && no_pair[0] == '1')) {
         int Bp = 128;
         while (Bp > 32 && p->ks.smem_v2p(n, Bp, !uniform) > smem_cap) Bp /= 2;
         const size_t smem_p = p->ks.smem_v2p(n, Bp, !uniform);
@@ -356,7 +369,9 @@ void plan_build(psa_plan* p, const psa_objective* f, const psa_engine_config* cf
     int per_sm = 0;
     cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, B, p->smem), "occupancy");
     if (per_sm < 1) fail(PSA_ERR_CUDA, "parsa_b200: engine kernel cannot be resident");
-    const long long units = p->pair ? (static_cast<long long>(p->chains_local) + 1) / 2 : p->chains_local;
+    const long long units = p->pc     ? (static_cast<long long>(p->chains_local) + 31) / 32 * B
+                            : p->pair ? (static_cast<long long>(p->chains_local) + 1) / 2
+                                      : p->chains_local;
     const long long need = (units + B - 1) / B;
     p->grid = static_cast<int>(std::min<long long>(need, static_cast<long long>(per_sm) * lim.sms));
     if (p->max_blocks > 0) p->grid = std::min(p->grid, p->max_blocks);
@@ -819,6 +834,7 @@ psa_status psa_plan_describe(const psa_plan* p, char* buf, int32_t capacity) {
                                                : p->hbm_rows ? "v1_kernel (HBM SoA rows)"
                                                              : "v1_kernel (shared-memory rows)")
                              : p->pair     ? "v2_pair_kernel (two chains per thread, shared-memory pair rows)"
+                             : p->pc       ? "v2_pc_kernel (producer/consumer warps, 32 chains per block)"
                              : p->hbm_rows ? "v2_kernel (HBM SoA rows)"
                                            : "v2_kernel (one chain per thread, shared-memory rows)";
         d << layout << " precision=" << (p->precision == PSA_F32 ? "f32" : "f64") << " family=" << p->family

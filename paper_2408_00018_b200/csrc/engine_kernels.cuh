@@ -131,6 +131,102 @@ struct RowSel<R, true> {
     }
 };
 
+// ---------------------------------------------------------------------------
+// Producer/consumer sweep for small chain counts (v2_pc_kernel)
+//
+// With few chains a level is one long dependency chain per thread: 100
+// trials of ~290 instructions each, with one warp per scheduler and nothing
+// to overlap.  But the proposals are independent of the chain's state
+// (counter-based streams), so other warps can make them: warps 1..3 of the
+// block compute every trial's coordinate, new cached term and acceptance
+// draw (the three Philox draws and the glibc-exact term — the bulk of a
+// trial's instructions) into a double-buffered shared-memory ring, 32
+// trials ahead, while warp 0 runs only what depends on the chain: slot
+// write, fold, Metropolis decision.  Each chain's draws, terms and decisions
+// are exactly those of sweep().
+// ---------------------------------------------------------------------------
+
+template <class R, int A>
+struct PcEntry {
+    uint64_t m; // acceptance draw (53-bit mantissa integer)
+    int32_t d;  // coordinate
+    R t[A];     // its new cached value(s)
+};
+
+// entries for trials [j0, j0 + jn) of the 32 chains of a group:
+// buf[trial][lane], filled by threads 32.. of the block
+template <class R, class Cost>
+__device__ void pc_produce(PcEntry<R, Cost::A>* buf, int j0, int jn, int n, uint32_t chain_base, uint32_t level,
+                           uint32_t ctr0, const Box& box, const PhiloxKeys& keys) {
+    const int p = static_cast<int>(threadIdx.x) - 32, np = static_cast<int>(blockDim.x) - 32;
+    const double idx_scale = static_cast<double>(n) * 0x1.0p-53;
+    for (int e = p; e < 32 * jn; e += np) {
+        const int lane = e & 31, jj = e >> 5;
+        const PhiloxChain pc = philox_chain(chain_base + lane, level, keys);
+        const uint32_t ctr = ctr0 + 3u * static_cast<uint32_t>(j0 + jj);
+        const uint64_t m1 = draw_bits53_fast(ctr, pc, keys);
+        const uint64_t m2 = draw_bits53_fast(ctr + 1, pc, keys);
+        PcEntry<R, Cost::A> en;
+        en.m = draw_bits53_fast(ctr + 2, pc, keys);
+        en.d = min(static_cast<int>(static_cast<double>(m1) * idx_scale), n - 1);
+        const double x = box.point(en.d, bits_to_uniform(m2));
+        bool ok;
+        Cost::cache_common(static_cast<R>(x), en.d, n, en.t, ok);
+        if (!ok) Cost::cache(static_cast<R>(x), en.d, n, en.t);
+        buf[jj * 32 + lane] = en;
+    }
+}
+
+template <class R, class Cost, int NT>
+__device__ R pc_sweep(R* row, int n_rt, int family, R E, double temperature, uint32_t chain_base, uint32_t level,
+                      uint32_t ctr0, int N, const Box& box, const PhiloxKeys& keys, uint32_t* mask,
+                      size_t mask_stride, bool live, PcEntry<R, Cost::A>* buf) {
+    constexpr int A = Cost::A;
+    const int n = NT > 0 ? NT : n_rt;
+    const float k2 = static_cast<float>(1.4426950408889634 / temperature); // log2(e) / T
+    const bool producer = threadIdx.x >= 32;
+    const int lane = threadIdx.x & 31;
+    const int rounds = (N + 31) / 32;
+    if (producer) pc_produce<R, Cost>(buf, 0, N < 32 ? N : 32, n, chain_base, level, ctr0, box, keys);
+    __syncthreads();
+    for (int k = 0; k < rounds; ++k) {
+        const int jn = N - 32 * k < 32 ? N - 32 * k : 32;
+        if (producer) {
+            if (k + 1 < rounds) {
+                const int j1 = 32 * (k + 1);
+                pc_produce<R, Cost>(buf + ((k + 1) & 1) * 1024, j1, N - j1 < 32 ? N - j1 : 32, n, chain_base, level,
+                                    ctr0, box, keys);
+            }
+        } else if (live) {
+            const PcEntry<R, A>* cur = buf + (k & 1) * 1024;
+            uint32_t word = 0;
+            for (int j = 0; j < jn; ++j) {
+                const PcEntry<R, A> en = cur[j * 32 + lane];
+                R to[A];
+#pragma unroll
+                for (int a = 0; a < A; ++a) {
+                    to[a] = row[en.d * A + a];
+                    row[en.d * A + a] = en.t[a];
+                }
+                const R trial = Cost::template energy<NT>(row, n, family);
+                int r = metropolis_fast<R>(trial, E, k2, en.m);
+                if (__any_sync(__activemask(), r < 0))
+                    if (r < 0) r = Accept<R>::exact(static_cast<double>(trial) - static_cast<double>(E), temperature, en.m);
+                if (r) {
+                    E = trial;
+                    word |= 1u << j;
+                } else {
+#pragma unroll
+                    for (int a = 0; a < A; ++a) row[en.d * A + a] = to[a];
+                }
+            }
+            mask[static_cast<size_t>(k) * mask_stride] = word;
+        }
+        __syncthreads();
+    }
+    return E;
+}
+
 // draw_random_start (engines.cpp:43-46): coordinate k uses draw k of (seed, c, 0)
 __device__ __forceinline__ double random_start_coord(const EngineArgs& a, const Box& box,
                                                      uint32_t c, int k) {
@@ -286,7 +382,7 @@ struct PairOf<SepCost<float, F>> {
     }
 };
 
-template <class R, class Cost, int NT, bool G, bool PAIR>
+template <class R, class Cost, int NT, bool G, bool PAIR, bool PC = false>
 __device__ __forceinline__ void v2_body(const EngineArgs& a) {
     constexpr int A = Cost::A;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -294,9 +390,11 @@ __device__ __forceinline__ void v2_body(const EngineArgs& a) {
     const int B = blockDim.x, tid = threadIdx.x;
     const int n = a.n;
     Smem sm{smem_raw};
-    // pair rows hold 2 n A interleaved values (chains A and B of the pair)
+    // pair rows hold 2 n A interleaved values (chains A and B of the pair);
+    // producer/consumer blocks keep rows for their consumer warp only
     const int S = G ? n * A : row_stride<R>(PAIR ? 2 * n : n, A);
-    R* V = G ? nullptr : sm.take<R>(static_cast<size_t>(S) * B);
+    R* V = G ? nullptr : sm.take<R>(static_cast<size_t>(S) * (PC ? 32 : B));
+    PcEntry<R, A>* pcbuf = PC ? sm.take<PcEntry<R, A>>(2 * 32 * 32) : nullptr;
     double* xs = sm.take<double>(n);
     R* vs = sm.take<R>(static_cast<size_t>(n) * A);
     double* lower = a.uniform_box ? nullptr : sm.take<double>(n);
@@ -329,7 +427,48 @@ __device__ __forceinline__ void v2_body(const EngineArgs& a) {
         const R estar = static_cast<R>(sh->estar);
         uint32_t* masks = a.masks + static_cast<size_t>(l & 1) * mask_buf;
         Cand best = empty_cand(), sbest = empty_cand();
-        if constexpr (PAIR) {
+        if constexpr (PC) {
+            // warp 0 consumes (one chain per lane), warps 1..3 produce the
+            // proposals; one group of 32 chains per block and round
+            const int lane = tid & 31;
+            const bool consumer = tid < 32;
+            for (size_t g = blockIdx.x; g * 32 < a.chains_local; g += gridDim.x) {
+                const size_t cl = g * 32 + lane;
+                const bool live = consumer && cl < a.chains_local;
+                const uint32_t c = static_cast<uint32_t>(a.chain_begin + (cl < a.chains_local ? cl : g * 32));
+                R* prow = V + static_cast<size_t>(lane) * S;
+                R e = 0;
+                uint32_t ctr = 0;
+                if (l == 0 && a.random_start) {
+                    if (live) {
+                        for (int k = 0; k < n; ++k) {
+                            R t[A];
+                            Cost::cache(static_cast<R>(random_start_coord(a, box, c, k)), k, n, t);
+#pragma unroll
+                            for (int q = 0; q < A; ++q) prow[k * A + q] = t[q];
+                        }
+                        e = Cost::template energy<NT>(prow, n, a.family);
+                        st.draws += static_cast<uint64_t>(n);
+                        const Cand s1{static_cast<double>(e), static_cast<int32_t>(c), 0};
+                        if (better(s1, sbest)) sbest = s1;
+                    }
+                    ctr = static_cast<uint32_t>(n);
+                } else if (live) {
+                    for (int k = 0; k < n * A; ++k) prow[k] = vs[k];
+                    e = estar;
+                }
+                if (l == 0 && live) st.evals += 1; // the start evaluation (engines.cpp:157)
+                e = pc_sweep<R, Cost, NT>(prow, n, a.family, e, temperature, static_cast<uint32_t>(a.chain_begin + g * 32),
+                                          static_cast<uint32_t>(l), ctr, a.N, box, a.keys, masks + cl, a.mask_stride,
+                                          live, pcbuf);
+                if (live) {
+                    st.evals += static_cast<uint64_t>(a.N);
+                    st.draws += 3ull * static_cast<uint64_t>(a.N);
+                    const Cand mine{static_cast<double>(e), static_cast<int32_t>(c), 0};
+                    if (better(mine, best)) best = mine;
+                }
+            }
+        } else if constexpr (PAIR) {
             // pair p = chains p and p + P (P = ceil(C/2)); an odd count leaves
             // the last pair's chain B a duplicate whose results are dropped
             // (its accept bits land in the padding columns of masks)
@@ -485,6 +624,13 @@ __device__ __forceinline__ void v2_body(const EngineArgs& a) {
 template <class R, class Cost, int NT, bool G>
 __global__ void __launch_bounds__(PSA_V2_MAX_THREADS, PSA_V2_MIN_BLOCKS) v2_kernel(const EngineArgs a) {
     v2_body<R, Cost, NT, G, false>(a);
+}
+
+// producer/consumer blocks for small chain counts: warp 0 consumes, warps
+// 1..3 produce (pc_sweep)
+template <class R, class Cost, int NT>
+__global__ void __launch_bounds__(128, 4) v2_pc_kernel(const EngineArgs a) {
+    v2_body<R, Cost, NT, false, false, true>(a);
 }
 
 // chain pairs: 800+ bytes of shared state per thread at n = 100 leave room
@@ -832,6 +978,11 @@ struct KernelSet {
         k.eval = reinterpret_cast<const void*>(&probe_evaluate<R, Cost>);
         k.sweep = reinterpret_cast<const void*>(&sweep_one<R, Cost>);
         k.smem_v2 = [](int n, int B, bool box) { return engine_smem_bytes<R, Cost::A>(n, B, box, true); };
+        k.v2pc = reinterpret_cast<const void*>(&v2_pc_kernel<R, Cost, NT>);
+        // rows for the consumer warp only, plus the 2 x 32 x 32 proposal ring
+        k.smem_v2pc = [](int n, int, bool box) {
+            return engine_smem_bytes<R, Cost::A>(n, 32, box, true) + 16 + sizeof(PcEntry<R, Cost::A>) * 2 * 32 * 32;
+        };
         if constexpr (PairOf<Cost>::value) {
             k.v1p = reinterpret_cast<const void*>(&v1_pair_kernel<R, Cost, NT>);
             k.v2p = reinterpret_cast<const void*>(&v2_pair_kernel<R, Cost, NT>);
