@@ -331,7 +331,12 @@ void plan_build(psa_plan* p, const psa_objective* f, const psa_engine_config* cf
     // Few chains (fewer than 8 warps per SM of one chain per thread): each
     // chain's level is a latency-bound dependency chain, so producer warps
     // take the proposals off its critical path (v2_pc_kernel).
-    const bool few = static_cast<long long>(p->chains_local) < 256ll * lim.sms;
+    // (Not for the families whose finish() runs transcendentals every trial —
+    // Ackley, exponential, Salomon: alone on the consumer's critical path
+    // they cost more than the producers save; measured on C3.)
+    const bool heavy_finish = p->family == PSA_FN_ACKLEY || p->family == PSA_FN_EXPONENTIAL ||
+                              p->family == PSA_FN_SALOMON;
+    const bool few = static_cast<long long>(p->chains_local) < 256ll * lim.sms && !heavy_finish;
     if (engine == 2 && !p->hbm_rows && p->ks.v2pc && (mode == "pc" || (mode.empty() && few)) &&
         p->ks.smem_v2pc(n, 128, !uniform) <= smem_cap) {
         p->pc = true;
