@@ -317,17 +317,10 @@ void plan_build(psa_plan* p, const psa_objective* f, const psa_engine_config* cf
     p->block = B;
     p->smem = p->hbm_rows ? p->ks.smem_g(n, B, !uniform) : smem_of(B);
     const void* kern = engine == 1 ? (p->hbm_rows ? p->ks.v1g : p->ks.v1) : (p->hbm_rows ? p->ks.v2g : p->ks.v2);
-    // binary32 separable families: two chains per thread (FADD2 fold) when
-    // the pair rows fit (PSA_NO_PAIR=1 keeps one chain per thread)
-    // V2 kernel choice (PSA_V2_MODE = single | pair overrides, for A/B
-    // measurements; both are bit-identical)
+    // Kernel choice (all variants are bit-identical; PSA_V2_MODE = single |
+    // pair | pc forces one for A/B measurements).
     const char* mode_env = std::getenv("PSA_V2_MODE");
     const std::string mode = mode_env ? mode_env : "";
-    const char* no_pair = std::getenv("PSA_NO_PAIR");
-    // Pairs halve the threads for the same chains, so they pay off only when
-    // the pair kernel still keeps >= 8 warps per SM resident and there are
-    // enough pairs to fill them (small chain counts or large n keep one chain
-    // per thread; PSA_V2_MODE=pair forces pairs whenever the rows fit).
     // Few chains (fewer than 8 warps per SM of one chain per thread): each
     // chain's level is a latency-bound dependency chain, so producer warps
     // take the proposals off its critical path (v2_pc_kernel).
@@ -344,9 +337,13 @@ void plan_build(psa_plan* p, const psa_objective* f, const psa_engine_config* cf
         p->smem = p->ks.smem_v2pc(n, 128, !uniform);
         kern = p->ks.v2pc;
     }
+    // Binary32 separable families: two chains per thread (FADD2 fold).
+    // Pairs halve the threads for the same chains, so they pay off only when
+    // the pair kernel still keeps >= 8 warps per SM resident and there are
+    // enough pairs to fill them (small chain counts or large n keep one chain
+    // per thread; PSA_V2_MODE=pair forces pairs whenever the rows fit).
     const void* pair_kern = engine == 2 ? p->ks.v2p : p->ks.v1p;
-    if (!p->pc && !p->hbm_rows && pair_kern && mode != "single" && mode != "pc" &&
-        !(no_pair && no_pair[0] == '1')) {
+    if (!p->pc && !p->hbm_rows && pair_kern && mode != "single" && mode != "pc") {
         int Bp = 128;
         while (Bp > 32 && p->ks.smem_v2p(n, Bp, !uniform) > smem_cap) Bp /= 2;
         const size_t smem_p = p->ks.smem_v2p(n, Bp, !uniform);

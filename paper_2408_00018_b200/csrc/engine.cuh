@@ -475,10 +475,7 @@ PSA_DEV void pair_energy(const float* row, int n_rt, float& eA, float& eB) {
         constexpr int M = NT * A;     // elements
         constexpr int NV = M / 2;     // 16-byte vectors
         const ulonglong2* p = reinterpret_cast<const ulonglong2*>(u);
-#ifndef PSA_PAIR_PREFETCH
-#define PSA_PAIR_PREFETCH 4
-#endif
-        constexpr int PF = PSA_PAIR_PREFETCH < NV ? PSA_PAIR_PREFETCH : NV;
+        constexpr int PF = 4 < NV ? 4 : NV; // vectors loaded ahead of the FADD2 chain
         ulonglong2 buf[PF > 0 ? PF : 1];
 #pragma unroll
         for (int q = 0; q < PF; ++q) buf[q] = p[q];
@@ -564,11 +561,9 @@ PSA_DEV void sweep_pair(float* row, int n_rt, float& EA, float& EB, double tempe
         bool okA, okB;
         Cost::cache_common(static_cast<float>(yA), nA, n, uA, okA);
         Cost::cache_common(static_cast<float>(yB), nB, n, uB, okB);
-#ifndef PSA_PAIR_NO_PIN
         asm volatile("" ::"l"(mA), "l"(mB), "r"(nA), "r"(nB));
 #pragma unroll
         for (int a = 0; a < A; ++a) asm volatile("" ::"f"(uA[a]), "f"(uB[a]));
-#endif
 
         float trA, trB;
         pair_energy<Fam, NT>(row, n, trA, trB);
