@@ -178,6 +178,14 @@ psa_status psa_run_synchronous(const psa_objective* f, const psa_engine_config* 
 /* nelder_mead_minimize, nelder_mead.cpp:37-115 */
 psa_status psa_nelder_mead_minimize(const psa_objective* f, const double* x_start,
                                     const psa_nm_config* nm, psa_nm_result* out);
+/* Batched nelder_mead_minimize (nelder_mead.cpp:37-115): `count`
+ * independent instances from x_starts (count x dim, row-major), one device
+ * thread each, every instance bit-identical to the reference's run from its
+ * start.  Outputs are caller-owned arrays of count (x_best: count x dim).
+ * For small dim (the simplex lives in per-thread global scratch). */
+psa_status psa_nelder_mead_batch(const psa_objective* f, const double* x_starts, int32_t count,
+                                 const psa_nm_config* nm, double* x_best, double* f_best,
+                                 int32_t* iterations, uint64_t* evaluations);
 /* hybrid_run, nelder_mead.cpp:117-136 */
 psa_status psa_hybrid_run(const psa_objective* f, const psa_engine_config* cfg,
                           const psa_schedule* truncated, const psa_nm_config* nm,

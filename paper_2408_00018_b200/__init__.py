@@ -33,6 +33,7 @@ from .api import (  # noqa: F401
     hybrid_run,
     ladder,
     location_error,
+    nelder_mead_batch,
     nelder_mead_minimize,
     reduce_min,
     registry,

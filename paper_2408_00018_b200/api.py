@@ -505,6 +505,27 @@ def nelder_mead_minimize(f: ObjectiveFunction, x_start: Sequence[float],
     return NelderMeadResult(xb.tolist(), r.f_best, r.iterations, r.evaluations)
 
 
+def nelder_mead_batch(f: ObjectiveFunction, x_starts, cfg: NelderMeadConfig = None) -> list:
+    """Many independent nelder_mead_minimize runs on the device, one thread
+    each (psa_nelder_mead_batch); each result is bit-identical to the
+    reference's run from that start.  x_starts: (count, dim) array-like."""
+    cfg = cfg or NelderMeadConfig()
+    lib = _lib()
+    X = np.ascontiguousarray(np.asarray(x_starts, dtype=np.float64).reshape(-1, f.dim))
+    m = X.shape[0]
+    xb = np.zeros((m, f.dim))
+    fb = np.zeros(m)
+    it = np.zeros(m, dtype=np.int32)
+    ev = np.zeros(m, dtype=np.uint64)
+    h = _Objective(f)
+    _raise(lib, lib.psa_nelder_mead_batch(C.byref(h.c), X.ctypes.data_as(C.POINTER(C.c_double)), m,
+                                          C.byref(cfg._c()), xb.ctypes.data_as(C.POINTER(C.c_double)),
+                                          fb.ctypes.data_as(C.POINTER(C.c_double)),
+                                          it.ctypes.data_as(C.POINTER(C.c_int32)),
+                                          ev.ctypes.data_as(C.POINTER(C.c_uint64))))
+    return [NelderMeadResult(list(xb[i]), float(fb[i]), int(it[i]), int(ev[i])) for i in range(m)]
+
+
 def hybrid_run(f: ObjectiveFunction, cfg: EngineConfig, truncated_sched: AnnealSchedule,
                nm_cfg: Optional[NelderMeadConfig] = None) -> RunResult:
     """nelder_mead.cpp:117-136: truncated synchronous SA, then the polish."""

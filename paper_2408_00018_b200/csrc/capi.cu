@@ -691,6 +691,71 @@ psa_status psa_nelder_mead_minimize(const psa_objective* f, const double* x_star
     return guarded([&] { nm_run(f, x_start, nm, out, nullptr); });
 }
 
+psa_status psa_nelder_mead_batch(const psa_objective* f, const double* x_starts, int32_t count,
+                                 const psa_nm_config* nm, double* x_best, double* f_best, int32_t* iterations,
+                                 uint64_t* evaluations) {
+    return guarded([&] {
+        if (!nm || (count > 0 && (!x_starts || !x_best || !f_best || !iterations || !evaluations)))
+            fail(PSA_ERR_INVALID_ARGUMENT, "parsa_b200: null argument");
+        if (count < 0) fail(PSA_ERR_INVALID_ARGUMENT, "parsa_b200: negative instance count");
+        validate_nm(*nm);
+        check_objective(f);
+        const int n = f->dim;
+        for (int32_t i = 0; i < count; ++i)
+            for (int k = 0; k < n; ++k) {
+                const double v = x_starts[static_cast<size_t>(i) * n + k];
+                if (v < f->lower[k] || v > f->upper[k])
+                    fail(PSA_ERR_INVALID_ARGUMENT, "nelder_mead_minimize: infeasible start");
+            }
+        if (count == 0) return;
+        require_device();
+        DevBuf<double> d_lo, d_hi, d_x0, d_scr, d_xb, d_fb;
+        DevBuf<int> d_ord, d_it;
+        DevBuf<unsigned long long> d_ev;
+        d_lo.alloc(n);
+        d_hi.alloc(n);
+        d_x0.alloc(static_cast<size_t>(count) * n);
+        d_scr.alloc(static_cast<size_t>(count) * psa::nm_batch_doubles(n));
+        d_ord.alloc(static_cast<size_t>(count) * (n + 1));
+        d_xb.alloc(static_cast<size_t>(count) * n);
+        d_fb.alloc(count);
+        d_it.alloc(count);
+        d_ev.alloc(count);
+        cuda_check(cudaMemcpy(d_lo.p, f->lower, sizeof(double) * n, cudaMemcpyHostToDevice), "H2D");
+        cuda_check(cudaMemcpy(d_hi.p, f->upper, sizeof(double) * n, cudaMemcpyHostToDevice), "H2D");
+        cuda_check(cudaMemcpy(d_x0.p, x_starts, sizeof(double) * count * n, cudaMemcpyHostToDevice), "H2D");
+        psa::NMBatchArgs a{};
+        a.n = n;
+        a.family = f->family;
+        a.max_iters = nm->max_iters > 0 ? nm->max_iters : 50000 * n;
+        a.count = count;
+        a.reflect = nm->reflect;
+        a.expand = nm->expand;
+        a.contract = nm->contract;
+        a.shrink = nm->shrink;
+        a.f_tol = nm->f_tol;
+        a.x_tol = nm->x_tol;
+        a.lower = d_lo.p;
+        a.upper = d_hi.p;
+        a.x_starts = d_x0.p;
+        a.scratch = d_scr.p;
+        a.order = d_ord.p;
+        a.x_best = d_xb.p;
+        a.f_best = d_fb.p;
+        a.iterations = d_it.p;
+        a.evaluations = d_ev.p;
+        void* params[] = {&a};
+        cuda_check(cudaLaunchKernel(psa::nm_batch_kernel_for(f->family), dim3((count + 127) / 128), dim3(128), params,
+                                    0, 0),
+                   "launch nm_batch_kernel");
+        cuda_check(cudaMemcpy(x_best, d_xb.p, sizeof(double) * count * n, cudaMemcpyDeviceToHost), "D2H");
+        cuda_check(cudaMemcpy(f_best, d_fb.p, sizeof(double) * count, cudaMemcpyDeviceToHost), "D2H");
+        cuda_check(cudaMemcpy(iterations, d_it.p, sizeof(int) * count, cudaMemcpyDeviceToHost), "D2H");
+        static_assert(sizeof(unsigned long long) == sizeof(uint64_t), "u64");
+        cuda_check(cudaMemcpy(evaluations, d_ev.p, sizeof(uint64_t) * count, cudaMemcpyDeviceToHost), "D2H");
+    });
+}
+
 psa_status psa_hybrid_run(const psa_objective* f, const psa_engine_config* cfg, const psa_schedule* truncated,
                           const psa_nm_config* nm, psa_run_result* out) {
     return guarded([&] {

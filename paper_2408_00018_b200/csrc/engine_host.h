@@ -90,6 +90,31 @@ struct NMArgsHost {
     NMOut* out;
 };
 
+// batched NM: one instance per thread (nm_batch_kernel)
+struct NMBatchArgs {
+    int n;
+    int family;
+    int max_iters;
+    int count;
+    double reflect, expand, contract, shrink, f_tol, x_tol;
+    const double* lower;
+    const double* upper;
+    const double* x_starts; // count x n
+    double* scratch;        // count x ((n+1)(n+1) + (4+A) n) doubles
+    int* order;             // count x (n+1)
+    double* x_best;         // count x n
+    double* f_best;         // count
+    int* iterations;        // count
+    unsigned long long* evaluations; // count
+};
+const void* nm_batch_kernel_for(int family);
+// scratch doubles per batched instance: vertices, values, centroid and three
+// trial points, cost terms (A <= 2)
+PSA_HD size_t nm_batch_doubles(int n) {
+    const size_t d = static_cast<size_t>(n + 1) * n + static_cast<size_t>(n + 1) + 6 * static_cast<size_t>(n);
+    return (d + 1) & ~size_t(1); // even: every instance's terms stay 16-byte aligned
+}
+
 struct EngineKernels {
     const void* v2;
     const void* v1;

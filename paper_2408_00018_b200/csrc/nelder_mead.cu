@@ -392,6 +392,147 @@ __global__ void __launch_bounds__(512) nm_kernel(const NMArgs a) {
     cluster.sync(); // no CTA may exit while others can still store into its shared memory
 }
 
+// ---------------------------------------------------------------------------
+// Batched Nelder–Mead: one independent instance per thread (small n).
+//
+// nelder_mead_minimize (nelder_mead.cpp:37-115) restated literally for one
+// thread — the O(n^2) centroid with a division per element, the clamped
+// trial points, std::sort through the libstdc++ introsort restatement
+// (parsa_stdsort.h) — so every instance equals the reference's run from its
+// start point bit for bit.  Used to polish many points at once (e.g. the
+// best chains of a run); scratch is instance-major global memory (L1/L2).
+// ---------------------------------------------------------------------------
+
+template <class Cost>
+__global__ void __launch_bounds__(128) nm_batch_kernel(const NMBatchArgs a) {
+    constexpr int A = Cost::A;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= a.count) return;
+    const int n = a.n;
+    const size_t per = nm_batch_doubles(n); // (host allocates count * per)
+    // terms first: the fold reads them with 16-byte loads (per is even)
+    double* terms = a.scratch + static_cast<size_t>(i) * per; // n*A (A <= 2)
+    double* X = terms + 2 * static_cast<size_t>(n);            // (n+1) x n vertices
+    double* F = X + static_cast<size_t>(n + 1) * n;            // n+1 values
+    double* cen = F + (n + 1);
+    double* xr = cen + n;
+    double* xe = xr + n;
+    double* xc = xe + n;
+    int* ord = a.order + static_cast<size_t>(i) * (n + 1);
+    const double* x0 = a.x_starts + static_cast<size_t>(i) * n;
+    unsigned long long evals = 0;
+    auto eval = [&](const double* x) {
+        for (int k = 0; k < n; ++k) {
+            double t[A];
+            Cost::cache(x[k], k, n, t);
+#pragma unroll
+            for (int q = 0; q < A; ++q) terms[k * A + q] = t[q];
+        }
+        ++evals;
+        return static_cast<double>(Cost::template energy<0>(terms, n, a.family));
+    };
+    auto vx = [&](int v) { return X + static_cast<size_t>(v) * n; };
+    // initial simplex (nelder_mead.cpp:50-59)
+    for (int v = 0; v <= n; ++v) {
+        double* x = vx(v);
+        for (int k = 0; k < n; ++k) x[k] = x0[k];
+        if (v > 0) {
+            const int k = v - 1;
+            const double step = 0.05 * (a.upper[k] - a.lower[k]);
+            x[k] = (x[k] + step <= a.upper[k]) ? x[k] + step : x[k] - step;
+        }
+        F[v] = eval(x);
+        ord[v] = v;
+    }
+    psa_std_sort(ord, n + 1, F);
+    int iter = 0;
+    for (; iter < a.max_iters; ++iter) {
+        // termination (:67-68) with simplex_diameter (:21-27)
+        double diam = 0;
+        const double* b = vx(ord[0]);
+        for (int v = 1; v <= n; ++v) {
+            const double* x = vx(ord[v]);
+            for (int k = 0; k < n; ++k) {
+                const double d = fabs(x[k] - b[k]);
+                diam = diam < d ? d : diam;
+            }
+        }
+        if (F[ord[n]] - F[ord[0]] <= a.f_tol || diam <= a.x_tol) break;
+        for (int k = 0; k < n; ++k) cen[k] = 0.0;
+        for (int v = 0; v < n; ++v) {
+            const double* x = vx(ord[v]);
+            for (int k = 0; k < n; ++k) cen[k] += x[k] / n;
+        }
+        const int w = ord[n];
+        const double* worst = vx(w);
+        const double worst_f = F[w];
+        for (int k = 0; k < n; ++k) xr[k] = clampd(cen[k] + a.reflect * (cen[k] - worst[k]), a.lower[k], a.upper[k]);
+        const double fr = eval(xr);
+        const double* src = nullptr;
+        double fs = 0;
+        if (fr < F[ord[0]]) {
+            for (int k = 0; k < n; ++k) xe[k] = clampd(cen[k] + a.expand * (xr[k] - cen[k]), a.lower[k], a.upper[k]);
+            const double fe = eval(xe);
+            src = fe < fr ? xe : xr;
+            fs = fe < fr ? fe : fr;
+        } else if (fr < F[ord[n - 1]]) {
+            src = xr;
+            fs = fr;
+        } else {
+            const bool outside = fr < worst_f;
+            for (int k = 0; k < n; ++k) {
+                const double toward = outside ? xr[k] : worst[k];
+                xc[k] = clampd(cen[k] + a.contract * (toward - cen[k]), a.lower[k], a.upper[k]);
+            }
+            const double fc = eval(xc);
+            if (fc < (outside ? fr : worst_f)) {
+                src = xc;
+                fs = fc;
+            } else {
+                // shrink towards the best vertex (:101-108)
+                const double* x0b = vx(ord[0]);
+                for (int v = 1; v <= n; ++v) {
+                    double* x = vx(ord[v]);
+                    for (int k = 0; k < n; ++k) x[k] = clampd(x0b[k] + a.shrink * (x[k] - x0b[k]), a.lower[k], a.upper[k]);
+                    F[ord[v]] = eval(x);
+                }
+            }
+        }
+        if (src) {
+            double* x = vx(w);
+            for (int k = 0; k < n; ++k) x[k] = src[k];
+            F[w] = fs;
+        }
+        psa_std_sort(ord, n + 1, F);
+    }
+    const double* b = vx(ord[0]);
+    for (int k = 0; k < n; ++k) a.x_best[static_cast<size_t>(i) * n + k] = b[k];
+    a.f_best[i] = F[ord[0]];
+    a.iterations[i] = iter;
+    a.evaluations[i] = evals;
+}
+
+template <class Cost>
+const void* nm_batch_ptr() {
+    return reinterpret_cast<const void*>(&nm_batch_kernel<Cost>);
+}
+
+const void* nm_batch_kernel_for(int family) {
+    switch (family) {
+    case PSA_FN_SCHWEFEL: return nm_batch_ptr<SepCost<double, Schwefel>>();
+    case PSA_FN_ACKLEY: return nm_batch_ptr<SepCost<double, Ackley>>();
+    case PSA_FN_COSINE_MIXTURE: return nm_batch_ptr<SepCost<double, CosineMixture>>();
+    case PSA_FN_EXPONENTIAL: return nm_batch_ptr<SepCost<double, Exponential>>();
+    case PSA_FN_GRIEWANK: return nm_batch_ptr<SepCost<double, Griewank>>();
+    case PSA_FN_MICHALEWICZ: return nm_batch_ptr<SepCost<double, Michalewicz>>();
+    case PSA_FN_RASTRIGIN: return nm_batch_ptr<SepCost<double, Rastrigin>>();
+    case PSA_FN_SALOMON: return nm_batch_ptr<SepCost<double, Salomon>>();
+    case PSA_FN_SHUBERT: return nm_batch_ptr<SepCost<double, Shubert>>();
+    case PSA_FN_SPHERE: return nm_batch_ptr<SepCost<double, Sphere>>();
+    default: return nm_batch_ptr<FullCost<double>>();
+    }
+}
+
 // shared memory of one CTA of an NM cluster of `cl` CTAs; with q_smem the
 // CTA also keeps its columns' quotients Q ((n+1) x ceil(n/cl)) and centroid
 // checkpoints (n/16+1 rows) in shared memory
