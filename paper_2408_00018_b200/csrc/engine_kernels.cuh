@@ -178,27 +178,40 @@ __device__ void pc_produce(PcEntry<R, Cost::A>* buf, int j0, int jn, int n, uint
 }
 
 template <class R, class Cost, int NT>
+//  slot: the ring slot (of 3) holding round 0 (updated for the next call);
+//  prefilled: round 0 is already there (made during the previous call);
+//  prefetch_next: make round 0 of the same chains' next level (counter 0,
+//  level + 1) ahead — during the second-to-last round when the last round
+//  is short (its few trials would leave the consumer nothing to overlap),
+//  else during the last round.
 __device__ R pc_sweep(R* row, int n_rt, int family, R E, double temperature, uint32_t chain_base, uint32_t level,
                       uint32_t ctr0, int N, const Box& box, const PhiloxKeys& keys, uint32_t* mask,
-                      size_t mask_stride, bool live, PcEntry<R, Cost::A>* buf) {
+                      size_t mask_stride, bool live, PcEntry<R, Cost::A>* buf, int& slot, bool prefilled,
+                      bool prefetch_next) {
     constexpr int A = Cost::A;
     const int n = NT > 0 ? NT : n_rt;
     const float k2 = static_cast<float>(1.4426950408889634 / temperature); // log2(e) / T
     const bool producer = threadIdx.x >= 32;
     const int lane = threadIdx.x & 31;
     const int rounds = (N + 31) / 32;
-    if (producer) pc_produce<R, Cost>(buf, 0, N < 32 ? N : 32, n, chain_base, level, ctr0, box, keys);
-    __syncthreads();
+    auto at = [&](int k) { return buf + ((slot + k) % 3) * 1024; }; // ring slot of round k
+    if (!prefilled) {
+        if (producer) pc_produce<R, Cost>(at(0), 0, N < 32 ? N : 32, n, chain_base, level, ctr0, box, keys);
+        __syncthreads();
+    }
+    const bool short_last = rounds > 1 && N - 32 * (rounds - 1) <= 16;
     for (int k = 0; k < rounds; ++k) {
         const int jn = N - 32 * k < 32 ? N - 32 * k : 32;
         if (producer) {
             if (k + 1 < rounds) {
                 const int j1 = 32 * (k + 1);
-                pc_produce<R, Cost>(buf + ((k + 1) & 1) * 1024, j1, N - j1 < 32 ? N - j1 : 32, n, chain_base, level,
-                                    ctr0, box, keys);
+                pc_produce<R, Cost>(at(k + 1), j1, N - j1 < 32 ? N - j1 : 32, n, chain_base, level, ctr0, box, keys);
             }
+            const bool early = short_last && k + 2 == rounds, late = !short_last && k + 1 == rounds;
+            if (prefetch_next && (early || late))
+                pc_produce<R, Cost>(at(rounds), 0, N < 32 ? N : 32, n, chain_base, level + 1, 0u, box, keys);
         } else if (live) {
-            const PcEntry<R, A>* cur = buf + (k & 1) * 1024;
+            const PcEntry<R, A>* cur = at(k);
             uint32_t word = 0;
             for (int j = 0; j < jn; ++j) {
                 const PcEntry<R, A> en = cur[j * 32 + lane];
@@ -224,6 +237,7 @@ __device__ R pc_sweep(R* row, int n_rt, int family, R E, double temperature, uin
         }
         __syncthreads();
     }
+    slot = (slot + rounds) % 3; // where a prefetched next round 0 went
     return E;
 }
 
@@ -332,8 +346,10 @@ static __device__ void exchange_level(const EngineArgs& a, double* xs, Cand& w, 
         const char* rec = a.mail_self + (slot0 + tid) * a.rec_stride;
         const long long t0 = clock64();
         while (ld_acquire_sys(reinterpret_cast<const unsigned long long*>(rec)) != tag) {
-            if (clock64() - t0 > a.spin_limit) {
-                atomicExch(a.error_flag, 1); // a peer never arrived: report instead of hanging
+            // a peer never arrived: report instead of hanging, and once the
+            // run is known to be broken stop waiting at the later levels
+            if (clock64() - t0 > a.spin_limit || *reinterpret_cast<volatile int*>(a.error_flag)) {
+                atomicExch(a.error_flag, 1);
                 break;
             }
         }
@@ -394,7 +410,7 @@ __device__ __forceinline__ void v2_body(const EngineArgs& a) {
     // producer/consumer blocks keep rows for their consumer warp only
     const int S = G ? n * A : row_stride<R>(PAIR ? 2 * n : n, A);
     R* V = G ? nullptr : sm.take<R>(static_cast<size_t>(S) * (PC ? 32 : B));
-    PcEntry<R, A>* pcbuf = PC ? sm.take<PcEntry<R, A>>(2 * 32 * 32) : nullptr;
+    PcEntry<R, A>* pcbuf = PC ? sm.take<PcEntry<R, A>>(3 * 32 * 32) : nullptr;
     double* xs = sm.take<double>(n);
     R* vs = sm.take<R>(static_cast<size_t>(n) * A);
     double* lower = a.uniform_box ? nullptr : sm.take<double>(n);
@@ -421,6 +437,8 @@ __device__ __forceinline__ void v2_body(const EngineArgs& a) {
     const size_t mask_buf = W * a.mask_stride;
     const auto row = RowSel<R, G>::make(V, S, a, gtid);
     SweepStats st{0, 0};
+    int pc_slot = 0;            // producer/consumer ring state (PC mode)
+    bool pc_prefilled = false;
 
     for (int l = 0; l < a.levels; ++l) {
         const double temperature = a.temps[l];
@@ -458,9 +476,14 @@ __device__ __forceinline__ void v2_body(const EngineArgs& a) {
                     e = estar;
                 }
                 if (l == 0 && live) st.evals += 1; // the start evaluation (engines.cpp:157)
+                // one chain group per block: the producers make the next
+                // level's first round during this level's last one
+                const bool one_group = static_cast<size_t>(gridDim.x) * 32 >= a.chains_local;
                 e = pc_sweep<R, Cost, NT>(prow, n, a.family, e, temperature, static_cast<uint32_t>(a.chain_begin + g * 32),
                                           static_cast<uint32_t>(l), ctr, a.N, box, a.keys, masks + cl, a.mask_stride,
-                                          live, pcbuf);
+                                          live, pcbuf, pc_slot, one_group && pc_prefilled,
+                                          one_group && l + 1 < a.levels);
+                pc_prefilled = one_group && l + 1 < a.levels;
                 if (live) {
                     st.evals += static_cast<uint64_t>(a.N);
                     st.draws += 3ull * static_cast<uint64_t>(a.N);
@@ -979,9 +1002,9 @@ struct KernelSet {
         k.sweep = reinterpret_cast<const void*>(&sweep_one<R, Cost>);
         k.smem_v2 = [](int n, int B, bool box) { return engine_smem_bytes<R, Cost::A>(n, B, box, true); };
         k.v2pc = reinterpret_cast<const void*>(&v2_pc_kernel<R, Cost, NT>);
-        // rows for the consumer warp only, plus the 2 x 32 x 32 proposal ring
+        // rows for the consumer warp only, plus the 3 x 32 x 32 proposal ring
         k.smem_v2pc = [](int n, int, bool box) {
-            return engine_smem_bytes<R, Cost::A>(n, 32, box, true) + 16 + sizeof(PcEntry<R, Cost::A>) * 2 * 32 * 32;
+            return engine_smem_bytes<R, Cost::A>(n, 32, box, true) + 16 + sizeof(PcEntry<R, Cost::A>) * 3 * 32 * 32;
         };
         if constexpr (PairOf<Cost>::value) {
             k.v1p = reinterpret_cast<const void*>(&v1_pair_kernel<R, Cost, NT>);
