@@ -330,12 +330,13 @@ void plan_build(psa_plan* p, const psa_objective* f, const psa_engine_config* cf
     const bool heavy_finish = p->family == PSA_FN_ACKLEY || p->family == PSA_FN_EXPONENTIAL ||
                               p->family == PSA_FN_SALOMON;
     const bool few = static_cast<long long>(p->chains_local) < 256ll * lim.sms && !heavy_finish;
-    if (engine == 2 && !p->hbm_rows && p->ks.v2pc && (mode == "pc" || (mode.empty() && few)) &&
-        p->ks.smem_v2pc(n, 128, !uniform) <= smem_cap) {
+    const void* pc_kern = engine == 2 ? p->ks.v2pc : p->ks.v1pc;
+    const size_t smem_pc = engine == 2 ? p->ks.smem_v2pc(n, 128, !uniform) : p->ks.smem_v1pc(n, 128, !uniform);
+    if (!p->hbm_rows && pc_kern && (mode == "pc" || (mode.empty() && few)) && smem_pc <= smem_cap) {
         p->pc = true;
         p->block = B = 128;
-        p->smem = p->ks.smem_v2pc(n, 128, !uniform);
-        kern = p->ks.v2pc;
+        p->smem = smem_pc;
+        kern = pc_kern;
     }
     // Binary32 separable families: two chains per thread (FADD2 fold).
     // Pairs halve the threads for the same chains, so they pay off only when
@@ -897,7 +898,8 @@ psa_status psa_plan_describe(const psa_plan* p, char* buf, int32_t capacity) {
     return guarded([&] {
         if (!p || !buf || capacity < 1) fail(PSA_ERR_INVALID_ARGUMENT, "parsa_b200: null argument");
         std::ostringstream d;
-        const char* layout = p->engine == 1 ? (p->pair       ? "v1_pair_kernel (two chains per thread, shared-memory pair rows)"
+        const char* layout = p->engine == 1 ? (p->pc         ? "v1_pc_kernel (producer/consumer warps, 32 chains per block)"
+                                               : p->pair       ? "v1_pair_kernel (two chains per thread, shared-memory pair rows)"
                                                : p->hbm_rows ? "v1_kernel (HBM SoA rows)"
                                                              : "v1_kernel (shared-memory rows)")
                              : p->pair     ? "v2_pair_kernel (two chains per thread, shared-memory pair rows)"

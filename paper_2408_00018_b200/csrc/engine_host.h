@@ -121,6 +121,8 @@ struct EngineKernels {
     const void* v2p; // chain pairs (binary32 separable families), or nullptr
     const void* v1p; // V1 with chain pairs, or nullptr
     const void* v2pc; // producer/consumer blocks (small chain counts)
+    const void* v1pc; // V1 producer/consumer blocks
+    size_t (*smem_v1pc)(int n, int B, bool box);
     size_t (*smem_v2pc)(int n, int B, bool box);
     size_t (*smem_v2p)(int n, int B, bool box); // pair rows (the same for V1 pairs)
     const void* v2g; // HBM chain-state layout (large n)

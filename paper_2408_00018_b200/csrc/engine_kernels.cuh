@@ -778,6 +778,188 @@ __global__ void __launch_bounds__(256) v1_kernel(const EngineArgs a) {
     }
 }
 
+// V1 with producer/consumer warps (small chain counts, §2.4b): warp 0 runs
+// 32 chains (one per lane) through the whole ladder, warps 1..3 make every
+// trial's proposal 32 trials ahead (pc_produce on stream (seed, c, 0), whose
+// counter runs on across levels).  The lanes move in lockstep, so each
+// level's trace candidate is a warp argmin; points of the chains are kept in
+// HBM and updated on accepted moves (the producers also store the proposed
+// coordinate value).
+template <class R, int A>
+struct PcEntryX {
+    PcEntry<R, A> p;
+    double x; // the proposed coordinate value (compute_neighbour)
+};
+
+template <class R, class Cost>
+__device__ void pc_produce_x(PcEntryX<R, Cost::A>* buf, long long j0, int jn, int n, uint32_t chain_base,
+                             uint32_t ctr0, const Box& box, const PhiloxKeys& keys) {
+    const int p = static_cast<int>(threadIdx.x) - 32, np = static_cast<int>(blockDim.x) - 32;
+    const double idx_scale = static_cast<double>(n) * 0x1.0p-53;
+    for (int e = p; e < 32 * jn; e += np) {
+        const int lane = e & 31, jj = e >> 5;
+        const PhiloxChain pc = philox_chain(chain_base + lane, 0u, keys);
+        const uint32_t ctr = ctr0 + 3u * static_cast<uint32_t>(j0 + jj);
+        const uint64_t m1 = draw_bits53_fast(ctr, pc, keys);
+        const uint64_t m2 = draw_bits53_fast(ctr + 1, pc, keys);
+        PcEntryX<R, Cost::A> en;
+        en.p.m = draw_bits53_fast(ctr + 2, pc, keys);
+        en.p.d = min(static_cast<int>(static_cast<double>(m1) * idx_scale), n - 1);
+        en.x = box.point(en.p.d, bits_to_uniform(m2));
+        bool ok;
+        Cost::cache_common(static_cast<R>(en.x), en.p.d, n, en.p.t, ok);
+        if (!ok) Cost::cache(static_cast<R>(en.x), en.p.d, n, en.p.t);
+        buf[jj * 32 + lane] = en;
+    }
+}
+
+template <class R, class Cost, int NT>
+__global__ void __launch_bounds__(128, 4) v1_pc_kernel(const EngineArgs a) {
+    constexpr int A = Cost::A;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int B = blockDim.x, tid = threadIdx.x, lane = tid & 31;
+    const int n = a.n;
+    Smem sm{smem_raw};
+    const int S = row_stride<R>(n, A);
+    R* V = sm.take<R>(static_cast<size_t>(S) * 32);
+    PcEntryX<R, A>* buf = sm.take<PcEntryX<R, A>>(2 * 32 * 32);
+    double* xs = sm.take<double>(n);
+    R* vs = sm.take<R>(static_cast<size_t>(n) * A);
+    double* lower = a.uniform_box ? nullptr : sm.take<double>(n);
+    double* width = a.uniform_box ? nullptr : sm.take<double>(n);
+    Cand* scratch = sm.take<Cand>(34);
+    SharedScalars* sh = sm.take<SharedScalars>(1);
+
+    Box box;
+    load_box<R, Cost>(a, lower, width, box);
+    for (int k = tid; k < n; k += B) xs[k] = a.start[k];
+    __syncthreads();
+    cache_point<R, Cost>(xs, vs, n, a.family);
+    __syncthreads();
+    if (tid == 0) sh->estar = static_cast<double>(Cost::template energy<NT>(vs, n, a.family));
+    __syncthreads();
+
+    const bool consumer = tid < 32, producer = !consumer;
+    const size_t gslot = static_cast<size_t>(blockIdx.x) * 32 + lane; // this lane's xrows / xbest slot
+    const size_t xst = a.threads;
+    double* xrow = a.xrows + gslot;
+    R* row = V + static_cast<size_t>(lane) * S;
+    const float* none = nullptr;
+    (void)none;
+    SweepStats st{0, 0};
+    Cand mybest = empty_cand();
+    const long long total = static_cast<long long>(a.levels) * a.N; // trials per chain
+    const int rounds = static_cast<int>((total + 31) / 32);
+
+    for (size_t g = blockIdx.x; g * 32 < a.chains_local; g += gridDim.x) {
+        const size_t cl = g * 32 + lane;
+        const bool live = consumer && cl < a.chains_local;
+        const uint32_t chain_base = static_cast<uint32_t>(a.chain_begin + g * 32);
+        const uint32_t c = static_cast<uint32_t>(a.chain_begin + (cl < a.chains_local ? cl : g * 32));
+        R e = 0;
+        uint32_t ctr0 = 0;
+        if (a.random_start) {
+            if (live) {
+                for (int k = 0; k < n; ++k) {
+                    const double xk = random_start_coord(a, box, c, k);
+                    xrow[k * xst] = xk;
+                    R t[A];
+                    Cost::cache(static_cast<R>(xk), k, n, t);
+#pragma unroll
+                    for (int q = 0; q < A; ++q) row[k * A + q] = t[q];
+                }
+                e = Cost::template energy<NT>(row, n, a.family);
+                st.draws += static_cast<uint64_t>(n);
+            }
+            ctr0 = static_cast<uint32_t>(n);
+        } else if (live) {
+            for (int k = 0; k < n; ++k) xrow[k * xst] = xs[k];
+            for (int k = 0; k < n * A; ++k) row[k] = vs[k];
+            e = static_cast<R>(sh->estar);
+        }
+        if (live) st.evals += 1;
+        double chain_best = static_cast<double>(e);
+        if (producer) pc_produce_x<R, Cost>(buf, 0, total < 32 ? static_cast<int>(total) : 32, n, chain_base, ctr0, box, a.keys);
+        __syncthreads();
+        int level = 0, in_level = 0; // the trial's level and position in it
+        float k2 = static_cast<float>(1.4426950408889634 / a.temps[0]);
+        for (int k = 0; k < rounds; ++k) {
+            const long long j0 = 32ll * k;
+            const int jn = total - j0 < 32 ? static_cast<int>(total - j0) : 32;
+            if (producer) {
+                if (k + 1 < rounds) {
+                    const long long j1 = j0 + 32;
+                    pc_produce_x<R, Cost>(buf + ((k + 1) & 1) * 1024, j1, total - j1 < 32 ? static_cast<int>(total - j1) : 32,
+                                          n, chain_base, ctr0, box, a.keys);
+                }
+            } else {
+                const PcEntryX<R, A>* cur = buf + (k & 1) * 1024;
+                for (int j = 0; j < jn; ++j) {
+                    if (live) {
+                        const PcEntryX<R, A> en = cur[j * 32 + lane];
+                        R to[A];
+#pragma unroll
+                        for (int q = 0; q < A; ++q) {
+                            to[q] = row[en.p.d * A + q];
+                            row[en.p.d * A + q] = en.p.t[q];
+                        }
+                        const R trial = Cost::template energy<NT>(row, n, a.family);
+                        const double T = a.temps[level];
+                        int r = metropolis_fast<R>(trial, e, k2, en.p.m);
+                        if (__any_sync(__activemask(), r < 0))
+                            if (r < 0) r = Accept<R>::exact(static_cast<double>(trial) - static_cast<double>(e), T, en.p.m);
+                        if (r) {
+                            e = trial;
+                            xrow[static_cast<size_t>(en.p.d) * xst] = en.x;
+                        } else {
+#pragma unroll
+                            for (int q = 0; q < A; ++q) row[en.p.d * A + q] = to[q];
+                        }
+                    }
+                    if (++in_level == a.N) {
+                        // level end (engines.cpp:90-106): std::min(chain_best, energy),
+                        // then the warp's trace candidate (NaN skipped)
+                        if (static_cast<double>(e) < chain_best) chain_best = static_cast<double>(e);
+                        Cand tv = live && !is_nan(chain_best) ? Cand{chain_best, static_cast<int32_t>(c), 0}
+                                                              : empty_cand();
+                        tv = warp_argmin(tv);
+                        if (lane == 0) {
+                            Cand* slot = &a.trace_cand[static_cast<size_t>(level) * gridDim.x + blockIdx.x];
+                            if (g == blockIdx.x || better(tv, *slot)) *slot = tv;
+                        }
+                        in_level = 0;
+                        if (++level < a.levels) k2 = static_cast<float>(1.4426950408889634 / a.temps[level]);
+                    }
+                }
+            }
+            __syncthreads();
+        }
+        if (live) {
+            st.evals += static_cast<uint64_t>(total);
+            st.draws += 3ull * static_cast<uint64_t>(total);
+            const Cand mine{static_cast<double>(e), static_cast<int32_t>(c), static_cast<int32_t>(gslot)};
+            if (better(mine, mybest)) {
+                mybest = mine;
+                for (int k = 0; k < n; ++k) a.xbest[gslot * static_cast<size_t>(n) + k] = xrow[k * xst];
+            }
+        }
+        __syncthreads();
+    }
+    const Cand b = block_argmin(mybest, scratch);
+    if (tid == 0) a.cand[blockIdx.x] = b;
+
+    __shared__ unsigned long long red_e, red_d;
+    if (tid == 0) { red_e = 0; red_d = 0; }
+    __syncthreads();
+    atomicAdd(&red_e, static_cast<unsigned long long>(st.evals));
+    atomicAdd(&red_d, static_cast<unsigned long long>(st.draws));
+    __syncthreads();
+    if (tid == 0) {
+        atomicAdd(&a.out_scalars->evaluations, red_e);
+        atomicAdd(&a.out_scalars->rng_draws, red_d);
+    }
+}
+
 // V1 with chain pairs (binary32 separable families): thread t runs chains p
 // and p + P (P = ceil(C/2)) through the whole ladder side by side
 // (sweep_pair), each on its own stream (seed, c, 0); per level the block
@@ -1002,6 +1184,10 @@ struct KernelSet {
         k.sweep = reinterpret_cast<const void*>(&sweep_one<R, Cost>);
         k.smem_v2 = [](int n, int B, bool box) { return engine_smem_bytes<R, Cost::A>(n, B, box, true); };
         k.v2pc = reinterpret_cast<const void*>(&v2_pc_kernel<R, Cost, NT>);
+        k.v1pc = reinterpret_cast<const void*>(&v1_pc_kernel<R, Cost, NT>);
+        k.smem_v1pc = [](int n, int, bool box) {
+            return engine_smem_bytes<R, Cost::A>(n, 32, box, true) + 16 + sizeof(PcEntryX<R, Cost::A>) * 2 * 32 * 32;
+        };
         // rows for the consumer warp only, plus the 3 x 32 x 32 proposal ring
         k.smem_v2pc = [](int n, int, bool box) {
             return engine_smem_bytes<R, Cost::A>(n, 32, box, true) + 16 + sizeof(PcEntry<R, Cost::A>) * 3 * 32 * 32;
