@@ -844,8 +844,6 @@ __global__ void __launch_bounds__(128, 4) v1_pc_kernel(const EngineArgs a) {
     const size_t xst = a.threads;
     double* xrow = a.xrows + gslot;
     R* row = V + static_cast<size_t>(lane) * S;
-    const float* none = nullptr;
-    (void)none;
     SweepStats st{0, 0};
     Cand mybest = empty_cand();
     const long long total = static_cast<long long>(a.levels) * a.N; // trials per chain
