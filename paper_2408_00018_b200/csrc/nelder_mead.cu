@@ -35,6 +35,7 @@
 #include "engine.cuh"
 #include "engine_host.h"
 #include "parsa_stdsort.h"
+#include "parsa_stdsort_pairs.hpp"
 
 namespace psa {
 
@@ -196,12 +197,19 @@ __global__ void __launch_bounds__(512) nm_kernel(const NMArgs a) {
     int* rk = ist + 4;         // n+1 ints: ranks of the full sort
     int* saved = rk + (n + 1); // n+1 ints: the pre-sort order
     auto equiv = [](double a, double b) { return !(a < b) && !(b < a); };
+    // (key, id) pairs for the exact sort: one 16-byte load per comparison
+    // instead of an id and then its key (the terms area is idle here)
+    psa_sort::KeyId* kp = reinterpret_cast<psa_sort::KeyId*>(terms);
     auto exact_sort = [&]() {
+        for (int p = tid; p <= n; p += B) kp[p] = psa_sort::KeyId{f_s[ord_s[p]], ord_s[p], 0};
+        __syncthreads();
         if (tid == 0) {
-            psa_std_sort(ord_s, n + 1, f_s);
+            psa_sort::sort(kp, n + 1);
             ist[0] = 0;
             ist[1] = -1;
         }
+        __syncthreads();
+        for (int p = tid; p <= n; p += B) ord_s[p] = kp[p].id;
         __syncthreads();
     };
     auto full_sort = [&]() {
