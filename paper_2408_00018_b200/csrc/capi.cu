@@ -562,8 +562,9 @@ void nm_run(const psa_objective* f, const double* x_start, const psa_nm_config* 
             fail(PSA_ERR_INVALID_ARGUMENT, "nelder_mead_minimize: infeasible start");
     require_device();
     const int max_iters = nm->max_iters > 0 ? nm->max_iters : 50000 * n;
-    DevBuf<double> d_lo, d_hi, d_x0, d_X, d_Q, d_P, d_xb;
+    DevBuf<double> d_lo, d_hi, d_x0, d_X, d_Q, d_P, d_T, d_xb;
     DevBuf<psa::NMOut> d_out;
+    const int ldt = 2 * n; // >= n * cached values per coordinate (<= 2), even: 16-byte aligned rows
     d_lo.alloc(n);
     d_hi.alloc(n);
     d_x0.alloc(n);
@@ -571,6 +572,7 @@ void nm_run(const psa_objective* f, const double* x_start, const psa_nm_config* 
     d_X.alloc(static_cast<size_t>(n + 1) * n);
     d_Q.alloc(static_cast<size_t>(n + 1) * n);
     d_P.alloc(static_cast<size_t>(n + 1) * n);
+    d_T.alloc(static_cast<size_t>(n + 1) * ldt);
     d_out.alloc(1);
     cuda_check(cudaMemcpy(d_lo.p, f->lower, sizeof(double) * n, cudaMemcpyHostToDevice), "H2D");
     cuda_check(cudaMemcpy(d_hi.p, f->upper, sizeof(double) * n, cudaMemcpyHostToDevice), "H2D");
@@ -591,6 +593,8 @@ void nm_run(const psa_objective* f, const double* x_start, const psa_nm_config* 
     a.X = d_X.p;
     a.Q = d_Q.p;
     a.P = d_P.p;
+    a.T = d_T.p;
+    a.ldt = ldt;
     a.x_best = d_xb.p;
     a.out = d_out.p;
     const void* k = psa::nm_kernel_for(f->family);

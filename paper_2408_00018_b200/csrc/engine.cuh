@@ -266,34 +266,57 @@ struct Accept<float> {
     }
 };
 
-// 2^x, MUFU.EX2 (relative error ~2^-22; subnormal results flush to 0)
-PSA_DEV float ex2_approx(float x) {
+// log2(x), MUFU.LG2 (absolute error below 2^-22 for normal x; 0 -> -inf)
+PSA_DEV float lg2_approx(float x) {
     float r;
-    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
     return r;
 }
 
-// The Metropolis decision (sa_core.cpp:46-55) with a branch-free pre-test;
-// returns 1 accept, 0 reject, -1 undecided.
+// The Metropolis decision (sa_core.cpp:46-55) with a branch-free pre-test in
+// the log domain; returns 1 accept, 0 reject, -1 undecided.
 //  * d = trial - E in R has the sign of the reference's double difference
 //    (subtracting two floats never flips the sign, is zero only for equal
 //    values, and is NaN exactly when the double one is; for R = double it
 //    is the reference's own difference), so d <= 0 is the downhill test.
-//  * e = 2^(-d * log2(e)/T) approximates exp(-dE/T) within a relative
-//    3e-5 wherever it is a normal float (|ln| <= 87.3: rounding of d, of the
-//    per-level factor k2 and of ex2.approx); the uniform (as the reference's
-//    float(u) = RN24(m)*2^-53, or u itself in f64 mode) is compared with e
-//    widened by 2^-12 either way.  Outside that band the answer is certain.
-//    When e flushes to zero, any m >= 1 rejects (the true value is below
-//    2^-125 < 2^-53); m == 0, NaNs and the band itself report undecided and
+//  * uphill, the reference accepts iff u <= exp(-dE/T), i.e. iff
+//    x = dE*log2(e)/T <= L = -log2(u).  The device forms x = float(d)*k2
+//    (k2 = log2(e)/T rounded to a normal float: relative error below 2^-22
+//    in all) and, from the acceptance draw alone, the band [lo, hi] =
+//    [L - 2^-10, L + 2^-10] with L = 53 - lg2.approx(float(m)) (MUFU.LG2's
+//    error, 2^-22 absolute, or even relative to |log2| <= 53, plus float(m)'s
+//    rounding stay below 2^-16 for u = m*2^-53, m >= 1; L <= 53).  x < lo accepts and
+//    x > hi rejects with certainty: the errors of x (|x| * 2^-22 < 2^-15 for
+//    |x| <= 60; a larger x is far beyond hi), of L, and of the reference's own
+//    exp / expf rounding and float(u) (relative 2^-23 each, below 2^-22 in
+//    the log domain) are all far inside the 2^-10 margin.  m == 0, NaNs, a
+//    k2 outside the normal floats and the band itself report undecided and
 //    the caller runs the exact glibc-restated test.
+//  * The band depends only on the draw, which the counter-based streams give
+//    ahead of the trial, so only an FADD, an FMUL and two compares follow the
+//    fold on the chain's critical path.
+struct MBand {
+    float lo, hi;
+};
+
+PSA_DEV MBand metropolis_band(uint64_t m) {
+    const float l = lg2_approx(__ull2float_rn(m));
+    const float nan = __int_as_float(0x7fffffff);
+    return MBand{m ? 0x1.a7fep+5f - l : nan, m ? 0x1.a802p+5f - l : nan}; // 53 -/+ 2^-10
+}
+
+// log2(e) / T as the pre-test's factor; NaN (always undecided) unless normal
+PSA_DEV float metropolis_k2(double temperature) {
+    const float k2 = static_cast<float>(1.4426950408889634 / temperature);
+    return (k2 >= 0x1.0p-126f && k2 <= 0x1.0p+126f) ? k2 : __int_as_float(0x7fffffff);
+}
+
 template <class R>
-PSA_DEV int metropolis_fast(R trial, R E, float k2, uint64_t m) {
+PSA_DEV int metropolis_fast(R trial, R E, float k2, MBand b) {
     const R d = trial - E;
-    const float e = ex2_approx(-static_cast<float>(d) * k2);
-    const float fm = __ull2float_rn(m);
-    const bool acc = (d <= R(0)) | (fm < e * 0x1.ffep+52f);  // 2^53 (1 - 2^-12)
-    const bool rej = fm > e * 0x1.001p+53f;                 // 2^53 (1 + 2^-12)
+    const float x = static_cast<float>(d) * k2;
+    const bool acc = (d <= R(0)) | (x < b.lo);
+    const bool rej = x > b.hi;
     return acc ? 1 : (rej ? 0 : -1);
 }
 
@@ -337,7 +360,7 @@ PSA_DEV R sweep(Row row, int n_rt, int family, R E, double temperature, uint32_t
                 uint32_t* mask, size_t mask_stride, double* x, size_t x_stride, SweepStats& st) {
     constexpr int A = Cost::A;
     const int n = NT > 0 ? NT : n_rt;
-    const float k2 = static_cast<float>(1.4426950408889634 / temperature); // log2(e) / T
+    const float k2 = metropolis_k2(temperature); // log2(e) / T
     const PhiloxChain pc = philox_chain(chain, level, keys);
     const double idx_scale = static_cast<double>(n) * 0x1.0p-53; // u*n == m*(n*2^-53) exactly
     // Two-stage software pipeline over the trials (the streams are counter-
@@ -382,10 +405,11 @@ PSA_DEV R sweep(Row row, int n_rt, int family, R E, double temperature, uint32_t
         const uint64_t r1 = draw_bits53_fast(ctr + 6, pc, keys);
         const uint64_t r2 = draw_bits53_fast(ctr + 7, pc, keys);
         const uint64_t r3 = draw_bits53_fast(ctr + 8, pc, keys);
+        const MBand b3 = metropolis_band(m3);
 #ifndef PSA_NO_PIN
         // materialise them here so the scheduler interleaves them into the
         // fold's FADD latency chain (left alone, the compiler sinks them)
-        asm volatile("" ::"l"(r1), "l"(r2), "l"(r3), "r"(dn));
+        asm volatile("" ::"l"(r1), "l"(r2), "l"(r3), "r"(dn), "f"(b3.lo), "f"(b3.hi));
 #pragma unroll
         for (int a = 0; a < A; ++a) {
             if constexpr (sizeof(R) == 4) asm volatile("" ::"f"(tnn[a]));
@@ -398,7 +422,7 @@ PSA_DEV R sweep(Row row, int n_rt, int family, R E, double temperature, uint32_t
             if (!ok) Cost::cache(static_cast<R>(xn), dn, n, tnn); // general path, practically never
 
         // sa_core.cpp:46-55 (the acceptance draw is consumed either way)
-        int r = metropolis_fast<R>(trial, E, k2, m3);
+        int r = metropolis_fast<R>(trial, E, k2, b3);
         if (__any_sync(__activemask(), r < 0))
             if (r < 0) r = Accept<R>::exact(static_cast<double>(trial) - static_cast<double>(E), temperature, m3);
         const bool acc = r != 0;
@@ -516,7 +540,7 @@ PSA_DEV void sweep_pair(float* row, int n_rt, float& EA, float& EB, double tempe
     using Cost = SepCost<float, F>;
     constexpr int A = Fam::kArrays;
     const int n = NT > 0 ? NT : n_rt;
-    const float k2 = static_cast<float>(1.4426950408889634 / temperature); // log2(e) / T
+    const float k2 = metropolis_k2(temperature); // log2(e) / T
     const PhiloxChain pa = philox_chain(cA, level, keys);
     const PhiloxChain pb = philox_chain(cB, level, keys);
     const double idx_scale = static_cast<double>(n) * 0x1.0p-53;
@@ -561,7 +585,8 @@ PSA_DEV void sweep_pair(float* row, int n_rt, float& EA, float& EB, double tempe
         bool okA, okB;
         Cost::cache_common(static_cast<float>(yA), nA, n, uA, okA);
         Cost::cache_common(static_cast<float>(yB), nB, n, uB, okB);
-        asm volatile("" ::"l"(mA), "l"(mB), "r"(nA), "r"(nB));
+        const MBand bA = metropolis_band(mA), bB = metropolis_band(mB);
+        asm volatile("" ::"f"(bA.lo), "f"(bA.hi), "f"(bB.lo), "f"(bB.hi), "r"(nA), "r"(nB));
 #pragma unroll
         for (int a = 0; a < A; ++a) asm volatile("" ::"f"(uA[a]), "f"(uB[a]));
 
@@ -573,8 +598,8 @@ PSA_DEV void sweep_pair(float* row, int n_rt, float& EA, float& EB, double tempe
             if (!okA) Cost::cache(static_cast<float>(yA), nA, n, uA);
             if (!okB) Cost::cache(static_cast<float>(yB), nB, n, uB);
         }
-        int rA = metropolis_fast<float>(trA, EA, k2, mA);
-        int rB = metropolis_fast<float>(trB, EB, k2, mB);
+        int rA = metropolis_fast<float>(trA, EA, k2, bA);
+        int rB = metropolis_fast<float>(trB, EB, k2, bB);
         if (__any_sync(__activemask(), (rA < 0) | (rB < 0))) {
             if (rA < 0) rA = Accept<float>::exact(static_cast<double>(trA) - static_cast<double>(EA), temperature, mA);
             if (rB < 0) rB = Accept<float>::exact(static_cast<double>(trB) - static_cast<double>(EB), temperature, mB);

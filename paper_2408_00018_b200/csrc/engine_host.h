@@ -86,6 +86,8 @@ struct NMArgsHost {
     double* X;      // (n+1) x n simplex storage (vertex-major)
     double* Q;      // (n+1) x n: Q[v][k] = X[v][k] / n, refreshed when vertex v changes
     double* P;      // (n+1) x n: P[p][k] = centroid prefix over the first p sorted vertices
+    double* T;      // (n+1) x ldt: cost terms of many vertices evaluated at once (start, shrink)
+    int ldt;        // even, >= n * (cached values per coordinate)
     double* x_best; // n
     NMOut* out;
 };

@@ -190,7 +190,7 @@ __device__ R pc_sweep(R* row, int n_rt, int family, R E, double temperature, uin
                       bool prefetch_next) {
     constexpr int A = Cost::A;
     const int n = NT > 0 ? NT : n_rt;
-    const float k2 = static_cast<float>(1.4426950408889634 / temperature); // log2(e) / T
+    const float k2 = metropolis_k2(temperature); // log2(e) / T
     const bool producer = threadIdx.x >= 32;
     const int lane = threadIdx.x & 31;
     const int rounds = (N + 31) / 32;
@@ -213,8 +213,13 @@ __device__ R pc_sweep(R* row, int n_rt, int family, R E, double temperature, uin
         } else if (live) {
             const PcEntry<R, A>* cur = at(k);
             uint32_t word = 0;
+            // entry j+1 is loaded at the top of trial j (before this trial's
+            // row stores, which the compiler cannot move it past), so its
+            // shared-memory latency is off the chain's critical path
+            PcEntry<R, A> nx = cur[lane];
             for (int j = 0; j < jn; ++j) {
-                const PcEntry<R, A> en = cur[j * 32 + lane];
+                const PcEntry<R, A> en = nx;
+                nx = cur[(j + 1 < jn ? j + 1 : j) * 32 + lane];
                 R to[A];
 #pragma unroll
                 for (int a = 0; a < A; ++a) {
@@ -222,7 +227,7 @@ __device__ R pc_sweep(R* row, int n_rt, int family, R E, double temperature, uin
                     row[en.d * A + a] = en.t[a];
                 }
                 const R trial = Cost::template energy<NT>(row, n, family);
-                int r = metropolis_fast<R>(trial, E, k2, en.m);
+                int r = metropolis_fast<R>(trial, E, k2, metropolis_band(en.m));
                 if (__any_sync(__activemask(), r < 0))
                     if (r < 0) r = Accept<R>::exact(static_cast<double>(trial) - static_cast<double>(E), temperature, en.m);
                 if (r) {
@@ -880,7 +885,7 @@ __global__ void __launch_bounds__(128, 4) v1_pc_kernel(const EngineArgs a) {
         if (producer) pc_produce_x<R, Cost>(buf, 0, total < 32 ? static_cast<int>(total) : 32, n, chain_base, ctr0, box, a.keys);
         __syncthreads();
         int level = 0, in_level = 0; // the trial's level and position in it
-        float k2 = static_cast<float>(1.4426950408889634 / a.temps[0]);
+        float k2 = metropolis_k2(a.temps[0]);
         for (int k = 0; k < rounds; ++k) {
             const long long j0 = 32ll * k;
             const int jn = total - j0 < 32 ? static_cast<int>(total - j0) : 32;
@@ -892,9 +897,11 @@ __global__ void __launch_bounds__(128, 4) v1_pc_kernel(const EngineArgs a) {
                 }
             } else {
                 const PcEntryX<R, A>* cur = buf + (k & 1) * 1024;
+                PcEntryX<R, A> nx = cur[lane]; // entry j+1 loaded during trial j (pc_sweep)
                 for (int j = 0; j < jn; ++j) {
+                    const PcEntryX<R, A> en = nx;
+                    nx = cur[(j + 1 < jn ? j + 1 : j) * 32 + lane];
                     if (live) {
-                        const PcEntryX<R, A> en = cur[j * 32 + lane];
                         R to[A];
 #pragma unroll
                         for (int q = 0; q < A; ++q) {
@@ -903,7 +910,7 @@ __global__ void __launch_bounds__(128, 4) v1_pc_kernel(const EngineArgs a) {
                         }
                         const R trial = Cost::template energy<NT>(row, n, a.family);
                         const double T = a.temps[level];
-                        int r = metropolis_fast<R>(trial, e, k2, en.p.m);
+                        int r = metropolis_fast<R>(trial, e, k2, metropolis_band(en.p.m));
                         if (__any_sync(__activemask(), r < 0))
                             if (r < 0) r = Accept<R>::exact(static_cast<double>(trial) - static_cast<double>(e), T, en.p.m);
                         if (r) {
@@ -926,7 +933,7 @@ __global__ void __launch_bounds__(128, 4) v1_pc_kernel(const EngineArgs a) {
                             if (g == blockIdx.x || better(tv, *slot)) *slot = tv;
                         }
                         in_level = 0;
-                        if (++level < a.levels) k2 = static_cast<float>(1.4426950408889634 / a.temps[level]);
+                        if (++level < a.levels) k2 = metropolis_k2(a.temps[level]);
                     }
                 }
             }
@@ -1134,7 +1141,7 @@ __global__ void sweep_one(const EngineArgs a, double* x, R* row, double* energy,
     }
     double E = *energy;
     unsigned long long ctr = *counter;
-    const float k2 = static_cast<float>(1.4426950408889634 / temperature); // log2(e) / T
+    const float k2 = metropolis_k2(temperature); // log2(e) / T
     for (int s = 0; s < n_steps; ++s) {
         const int d = coordinate_index(bits_to_uniform(draw_bits53(ctr, chain, level, a.keys)), n);
         const double xv = box.point(d, bits_to_uniform(draw_bits53(ctr + 1, chain, level, a.keys)));
@@ -1150,7 +1157,7 @@ __global__ void sweep_one(const EngineArgs a, double* x, R* row, double* energy,
         const double trial = static_cast<double>(Cost::template energy<0>(row, n, a.family));
         const uint64_t m3 = draw_bits53(ctr + 2, chain, level, a.keys);
         ctr += 3;
-        int r = metropolis_fast<double>(trial, E, k2, m3);
+        int r = metropolis_fast<double>(trial, E, k2, metropolis_band(m3));
         if (r < 0) r = Accept<R>::exact(trial - E, temperature, m3);
         if (r) {
             E = trial;

@@ -162,27 +162,44 @@ __global__ void __launch_bounds__(512) nm_kernel(const NMArgs a) {
         }
     };
 
-    // initial simplex (nelder_mead.cpp:50-59)
-    for (int v = 0; v <= n; ++v) {
-        for (int j = tid; j < nc; j += B) {
-            const int k = c0 + j;
-            double xk = a.x_start[k];
-            if (v > 0 && k == v - 1) {
-                const double step = 0.05 * (a.upper[k] - a.lower[k]);
-                xk = (xk + step <= a.upper[k]) ? xk + step : xk - step;
-            }
-            xr[j] = xk;
+    // f of many vertices at once (the initial simplex, a shrink): the caller
+    // has stored the terms of vertex list[first + i] (or first + i) into row i
+    // of T (global memory, L2-resident); the cluster's threads then fold one
+    // row each — the same index-order fold as eval(), for every vertex in
+    // parallel instead of one after another — and store each value into every
+    // CTA's f_s.
+    auto eval_rows = [&](int first, int count, const int* list) {
+        __threadfence();
+        csync();
+        for (int i = rank * B + tid; i < count; i += CL * B) {
+            const double f = Cost::template energy<0>(a.T + static_cast<size_t>(i) * a.ldt, n, a.family);
+            const int v = list ? list[first + i] : first + i;
+            for (int r = 0; r < CL; ++r) cluster.map_shared_rank(f_s, r)[v] = f;
         }
-        __syncthreads();
-        set_vertex(v, xr);
-        const double fv = eval(xr);
-        if (tid == 0) {
-            f_s[v] = fv;
-            ord_s[v] = v;
+        csync();
+    };
+    auto put_terms = [&](int row, int j, double x) { // row `row` of T, own column j
+        double t[A];
+        Cost::cache(x, c0 + j, n, t);
+#pragma unroll
+        for (int q = 0; q < A; ++q) a.T[static_cast<size_t>(row) * a.ldt + static_cast<size_t>(c0 + j) * A + q] = t[q];
+    };
+
+    // initial simplex (nelder_mead.cpp:50-59): n+1 independent evaluations
+    for (int idx = tid; idx < (n + 1) * nc; idx += B) {
+        const int v = idx / nc, j = idx - v * nc, k = c0 + j;
+        double xk = a.x_start[k];
+        if (v > 0 && k == v - 1) {
+            const double step = 0.05 * (a.upper[k] - a.lower[k]);
+            xk = (xk + step <= a.upper[k]) ? xk + step : xk - step;
         }
-        ++evals;
-        __syncthreads();
+        col(v, j) = xk;
+        Qb[static_cast<size_t>(v) * qst + j] = xk / dn;
+        put_terms(v, j, xk);
     }
+    for (int v = tid; v <= n; v += B) ord_s[v] = v;
+    eval_rows(0, n + 1, nullptr);
+    evals += n + 1;
     for (int j = tid; j < nc; j += B) Pb[j] = 0.0; // P[0] = the centroid's 0.0 fill
     if (tid == 0) {
         ist[0] = 0;  // valid centroid prefix length
@@ -371,20 +388,20 @@ __global__ void __launch_bounds__(512) nm_kernel(const NMArgs a) {
                 replace_worst(xc, fc);
             } else {
                 // shrink towards the best vertex (nelder_mead.cpp:101-108)
+                // (each new vertex depends only on itself and the best one,
+                // so all n are built and evaluated at once)
                 const int best = ord_s[0];
-                for (int i = 1; i <= n; ++i) {
-                    const int v = ord_s[i];
-                    for (int j = tid; j < nc; j += B) {
-                        const double x0 = col(best, j);
-                        xr[j] = clampd(x0 + a.shrink * (col(v, j) - x0), a.lower[c0 + j], a.upper[c0 + j]);
-                    }
-                    __syncthreads();
-                    set_vertex(v, xr);
-                    const double fv = eval(xr);
-                    ++evals;
-                    if (tid == 0) f_s[v] = fv;
-                    __syncthreads();
+                for (int idx = tid; idx < n * nc; idx += B) {
+                    const int i = idx / nc, j = idx - i * nc;
+                    const int v = ord_s[i + 1];
+                    const double x0 = col(best, j);
+                    const double xv = clampd(x0 + a.shrink * (col(v, j) - x0), a.lower[c0 + j], a.upper[c0 + j]);
+                    col(v, j) = xv;
+                    Qb[static_cast<size_t>(v) * qst + j] = xv / dn;
+                    put_terms(i, j, xv);
                 }
+                eval_rows(1, n, ord_s);
+                evals += n;
                 full_sort();
             }
         }
