@@ -170,4 +170,62 @@ PSA_PAIR_FN void sort(KeyId* v, int m) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// The same sort as independent tasks (the device runs one task per lane).
+//
+// introsort_loop only ever works on disjoint ranges: a range larger than the
+// threshold is either heap-sorted (depth budget spent) or split at a cut, and
+// its two halves never interact again.  The final insertion sort cannot move
+// an element across a cut either: everything left of a cut is not greater
+// than the pivot and everything right of it not less (keys without NaN are
+// strictly weakly ordered), and insertion only moves an element past a
+// strictly greater one.  So running, for every range as soon as it exists,
+// heap_sort / split and insertion_sort on every final range of at most
+// PSA_SORT_THRESHOLD elements gives the order of sort() exactly, in any task
+// order.  (Keys containing NaN take sort() itself.)
+// ---------------------------------------------------------------------------
+
+// one introsort_loop step on [first, last) with depth > 0: the cut
+PSA_PAIR_FN int split(KeyId* v, int first, int last) {
+    const int mid = first + (last - first) / 2;
+    median_to_first(v, first, first + 1, mid, last - 1);
+    return unguarded_partition(v, first + 1, last, first);
+}
+
+// the task of range [first, last) (size > threshold): calls emit(f, l, d)
+// for each child range still above the threshold and insertion-sorts the rest
+template <class Emit>
+PSA_PAIR_FN void range_task(KeyId* v, int first, int last, int depth, Emit&& emit) {
+    if (depth == 0) {
+        heap_sort(v, first, last);
+        return;
+    }
+    const int cut = split(v, first, last);
+    if (cut - first > PSA_SORT_THRESHOLD) emit(first, cut, depth - 1);
+    else insertion_sort(v, first, cut);
+    if (last - cut > PSA_SORT_THRESHOLD) emit(cut, last, depth - 1);
+    else insertion_sort(v, cut, last);
+}
+
+#if !defined(__CUDA_ARCH__)
+// host emulation of the task form, breadth first (tests)
+inline void sort_tasks(KeyId* v, int m) {
+    if (m <= PSA_SORT_THRESHOLD) {
+        insertion_sort(v, 0, m);
+        return;
+    }
+    struct R { int f, l, d; };
+    R cur[4096], nxt[4096];
+    int nc = 1;
+    cur[0] = R{0, m, psa_lg(m) * 2};
+    while (nc > 0) {
+        int nn = 0;
+        for (int i = nc - 1; i >= 0; --i) // any order: process the level backwards
+            range_task(v, cur[i].f, cur[i].l, cur[i].d, [&](int f, int l, int d) { nxt[nn++] = R{f, l, d}; });
+        for (int i = 0; i < nn; ++i) cur[i] = nxt[i];
+        nc = nn;
+    }
+}
+#endif
+
 } // namespace psa_sort

@@ -65,6 +65,38 @@ __device__ __forceinline__ double clampd(double v, double lo, double hi) {
 // the termination test max-reduces CL partials through DSMEM.
 // ---------------------------------------------------------------------------
 
+// The exact introsort's task form on warp 0 (psa_sort::range_task: one lane
+// per disjoint range, level by level; see parsa_stdsort_pairs.hpp).  Range
+// lists: cur / nxt, 3 ints per range; *count: the next level's length.  Not
+// inlined: its registers would otherwise be charged to the whole NM kernel.
+static __device__ __noinline__ void exact_sort_tasks(psa_sort::KeyId* kp, int m, int* cur, int* nxt, int* count) {
+    const int lane = threadIdx.x & 31;
+    if (lane == 0) {
+        cur[0] = 0;
+        cur[1] = m;
+        cur[2] = psa_lg(m) * 2;
+    }
+    int cnt = 1;
+    __syncwarp();
+    while (cnt > 0) {
+        if (lane == 0) *count = 0;
+        __syncwarp();
+        for (int i = lane; i < cnt; i += 32)
+            psa_sort::range_task(kp, cur[3 * i], cur[3 * i + 1], cur[3 * i + 2], [&](int f, int l, int d) {
+                const int k = atomicAdd(count, 1);
+                nxt[3 * k] = f;
+                nxt[3 * k + 1] = l;
+                nxt[3 * k + 2] = d;
+            });
+        __syncwarp();
+        cnt = *count;
+        __syncwarp();
+        int* t = cur;
+        cur = nxt;
+        nxt = t;
+    }
+}
+
 template <class Cost>
 __global__ void __launch_bounds__(512) nm_kernel(const NMArgs a) {
     constexpr int A = Cost::A;
@@ -210,18 +242,33 @@ __global__ void __launch_bounds__(512) nm_kernel(const NMArgs a) {
     // sorts in parallel (rank sort, or one insertion after replacing the worst
     // vertex); if any two values are equivalent (equal or NaN) the order of
     // the tied vertices is what libstdc++'s introsort makes of the physical
-    // order, so thread 0 runs that exact algorithm (parsa_stdsort.h).
+    // order, so the block runs that exact algorithm (parsa_stdsort.h).
     int* rk = ist + 4;         // n+1 ints: ranks of the full sort
     int* saved = rk + (n + 1); // n+1 ints: the pre-sort order
     auto equiv = [](double a, double b) { return !(a < b) && !(b < a); };
     // (key, id) pairs for the exact sort: one 16-byte load per comparison
     // instead of an id and then its key (the terms area is idle here)
     psa_sort::KeyId* kp = reinterpret_cast<psa_sort::KeyId*>(terms);
+    // Without NaN keys warp 0 runs the sort's task form (psa_sort::range_task:
+    // the introsort's disjoint ranges one per lane, level by level; the same
+    // order as sort(), see parsa_stdsort_pairs.hpp); with NaNs thread 0 runs
+    // sort() itself.  Range lists: rk / saved (idle here), 3 ints per range.
     auto exact_sort = [&]() {
-        for (int p = tid; p <= n; p += B) kp[p] = psa_sort::KeyId{f_s[ord_s[p]], ord_s[p], 0};
-        __syncthreads();
+        int has_nan = 0;
+        for (int p = tid; p <= n; p += B) {
+            const double fk = f_s[ord_s[p]];
+            kp[p] = psa_sort::KeyId{fk, ord_s[p], 0};
+            has_nan |= fk != fk;
+        }
+#ifdef PSA_NM_SEQ_SORT
+        has_nan = 1; // A/B builds: always the one-thread sort
+#endif
+        if (__syncthreads_or(has_nan) || n + 1 <= PSA_SORT_THRESHOLD) {
+            if (tid == 0) psa_sort::sort(kp, n + 1);
+        } else if (tid < 32) {
+            exact_sort_tasks(kp, n + 1, rk, saved, &ist[2]);
+        }
         if (tid == 0) {
-            psa_sort::sort(kp, n + 1);
             ist[0] = 0;
             ist[1] = -1;
         }
