@@ -52,7 +52,10 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--precision", default="f32", choices=["f32", "f64"])
-    ap.add_argument("--chains", type=int, default=CHAINS_PER_GPU, help="chains per GPU")
+    ap.add_argument("--chains", type=int, default=CHAINS_PER_GPU, help="chains per GPU (weak scaling)")
+    ap.add_argument("--chains-total", type=int, default=0,
+                    help="fixed total chain count sharded over the GPUs (strong scaling; configs[4] = 2^23)")
+    ap.add_argument("--no-configs", action="store_true", help="skip the C1/C3/C4 per-config entries")
     ap.add_argument("--tmin", type=float, default=SCHEDULE[1], help="override Tmin (shorter ladder)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-companion", action="store_true", help="skip the other-precision companion run")
@@ -150,6 +153,8 @@ def reference_sample(precision: int, seconds: float):
     rate = res.c.evaluations / wall
     sample = (f"parsa_ref::run_synchronous, Schwefel n=100, {chains} chains, schedule (1000, {tmin2:.3f}, 0.99, 100) "
               f"= first 2 levels of the paper ladder, {res.c.evaluations} evaluations in {wall:.2f} s")
+    reference_sample.last = {"chains": chains, "schedule": (SCHEDULE[0], tmin2, SCHEDULE[2], SCHEDULE[3]),
+                             "precision": precision, "result": res.as_dict()}
     return rate, sample, threads, chains, res.c.evaluations, wall
 
 
@@ -181,6 +186,125 @@ def run_reference_arm(args):
     print(json.dumps(line), flush=True)
 
 
+
+# ---------------------------------------------------------------------------
+# the other BASELINE.json configurations, timed once each after C2 (N=1)
+# ---------------------------------------------------------------------------
+
+# cached values per coordinate (objectives.cuh kArrays): the fold reads
+# 4*A*n (f32) / 8*A*n (f64) bytes of shared memory per trial
+ARRAYS = {"F0_a": 1, "F1_a": 2, "F13_a": 1}
+
+
+def _smem_peak():
+    try:
+        return float(json.load(open(os.path.join(ROOT, "profiles", "simt_peaks.json")))["smem_bytes_per_s"])
+    except (OSError, KeyError, ValueError):
+        return 148 * 128 * 1.965e9
+
+
+def _time_plan(psa, torch, f, cfg, engine, flush, reps):
+    stream = torch.cuda.current_stream()
+    sh = stream.cuda_stream
+    with psa.Plan(f, cfg, engine=engine) as p:
+        p.launch(sh)  # warm-up
+        p.fetch(sh)
+        ms = []
+        for _ in range(reps):
+            flush.fill_(1.0)
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            p.launch(sh)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms.append(e0.elapsed_time(e1))
+        r = p.fetch(sh)
+        return r, statistics.median(ms), p.description, p.launches_per_run
+
+
+def measure_configs(psa, torch, flush):
+    """C1, C3 (V1 and V2) and the C4 SA phase as device-timed entries (CUDA
+    events on the launch stream, L2 flushed before each timed launch), each
+    with its kernel and its fraction of the shared-memory roofline; plus the
+    C4 Nelder-Mead phase (per-iteration time at n=500 from the SA best)."""
+    paper = psa.AnnealSchedule(1000.0, 0.01, 0.99, 100)
+    peak = _smem_peak()
+    out = []
+
+    def entry(cname, workload, fid, f, cfg, engine, reps):
+        r, ms, desc, launches = _time_plan(psa, torch, f, cfg, engine, flush, reps)
+        assert r.evaluations == psa.expected_evaluations(cfg.schedule, cfg.n_chains)
+        trials = r.evaluations - cfg.n_chains
+        bpt = (4 if cfg.precision == psa.Precision.f32 else 8) * ARRAYS[fid] * f.dim
+        bw = trials * bpt / (ms / 1e3)
+        out.append({"config": cname, "workload": workload, "engine": {1: "v1", 2: "v2"}[engine],
+                    "function": fid, "n": f.dim, "chains": cfg.n_chains, "levels": len(r.trace),
+                    "dtype": cfg.precision.name, "evaluations": r.evaluations, "ms": ms,
+                    "value": r.evaluations / (ms / 1e3), "unit": UNIT, "kernel": desc, "launches": launches,
+                    "roofline": {"bound": "smem", "algorithmic_bytes_per_trial": bpt, "achieved": bw / 1e9,
+                                 "peak": peak / 1e9, "unit": "GB/s", "frac": bw / peak},
+                    "best_f": r.best_f, "winning_chain": r.winning_chain})
+        return r
+
+    schw = psa.registry_get("F0_a")
+    for prec in (psa.Precision.f32, psa.Precision.f64):
+        entry("C1", "configs[0]: synchronous SA, Schwefel n=10, 1024 chains, paper ladder", "F0_a",
+              schw.with_dim(10), psa.EngineConfig(n_chains=1024, schedule=paper, precision=prec), 2, 3)
+    for fid in ("F0_a", "F1_a", "F13_a"):
+        f = psa.registry_get(fid)
+        f = f if f.dim == 30 else f.with_dim(30)
+        for engine in (1, 2):
+            entry("C3", "configs[2]: V1 vs V2 on the suite, n=30, 16384 chains, paper ladder", fid, f,
+                  psa.EngineConfig(n_chains=16384, schedule=paper, precision=psa.Precision.f32), engine, 3)
+    trunc = psa.AnnealSchedule(1000.0, 32.0, 0.9, 100)
+    f500 = schw.with_dim(500)
+    r = None
+    for prec in (psa.Precision.f32, psa.Precision.f64):
+        rr = entry("C4-SA", "configs[3]: hybrid SA phase, Schwefel n=500, 2^20 chains, (1000, 32, 0.9, 100)",
+                   "F0_a", f500, psa.EngineConfig(n_chains=1 << 20, schedule=trunc, precision=prec), 2, 1)
+        r = rr if r is None else r
+    # Nelder-Mead phase (always f64) from the SA phase's best point, capped
+    iters = 20000
+    t0 = time.perf_counter()
+    nm = psa.nelder_mead_minimize(f500, r.best_x, psa.NelderMeadConfig(max_iters=iters))
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    out.append({"config": "C4-NM", "workload": "configs[3]: Nelder-Mead phase, n=500, from the SA best, "
+                f"{iters}-iteration cap", "kernel": "nm_kernel (16-CTA cluster)", "iterations": nm.iterations,
+                "evaluations": nm.evaluations, "ms": dt * 1e3, "us_per_iteration": dt * 1e6 / max(1, nm.iterations),
+                "f_best": nm.f_best, "note": "wall time of psa_nelder_mead_minimize (host buffers, one launch)"})
+    return out
+
+
+def parity_vs_reference(psa, f):
+    """Run the device on the exact sample the reference just ran for
+    cpu_baseline (same chains, schedule, precision, seed) and compare the
+    results bit for bit."""
+    last = getattr(reference_sample, "last", None)
+    if not last:
+        return None
+    import numpy as np
+
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle_lib import same_run
+
+    t0, tmin, rho, n = last["schedule"]
+    prec = psa.Precision.f32 if last["precision"] == 1 else psa.Precision.f64
+    cfg = psa.EngineConfig(n_chains=last["chains"], schedule=psa.AnnealSchedule(t0, tmin, rho, n), precision=prec)
+    with psa.Plan(f, cfg) as p:
+        p.launch(0)
+        r = p.fetch(0)
+        kernel = p.description
+    mine = {"best_x": np.array(r.best_x), "best_f": r.best_f, "evaluations": r.evaluations,
+            "winning_chain": r.winning_chain, "rng_draws": r.rng_draws, "trace_len": len(r.trace),
+            "trace": [(t.level, t.cumulative_evals, t.best_f) for t in r.trace]}
+    diff = same_run(mine, last["result"])
+    return {"against": "oracle/_ref parsa_ref::run_synchronous on the cpu_baseline sample", "chains": last["chains"],
+            "schedule": list(last["schedule"]), "dtype": prec.name, "kernel": kernel, "bitwise_equal": not diff,
+            "differing_fields": diff, "best_f": r.best_f, "winning_chain": r.winning_chain}
+
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
@@ -208,8 +332,16 @@ def main():
         raise SystemExit("bench: no sm_100 device visible (the library has no CPU fallback)")
 
     prec = psa.Precision.f32 if args.precision == "f32" else psa.Precision.f64
-    chains_per_gpu = args.chains
-    total_chains = chains_per_gpu * world
+    if args.chains_total > 0:  # strong scaling: a fixed global run sharded over the GPUs
+        from paper_2408_00018_b200.dist import shard_range
+
+        total_chains = args.chains_total
+        b, e = shard_range(total_chains, rank, world)
+        chains_per_gpu = e - b
+    else:  # weak scaling: a fixed chain count per GPU
+        chains_per_gpu = args.chains
+        total_chains = chains_per_gpu * world
+    scaling = "strong" if args.chains_total > 0 else "weak"
     sched = psa.AnnealSchedule(SCHEDULE[0], args.tmin, SCHEDULE[2], SCHEDULE[3])
     f = psa.registry_get("F0_a").with_dim(N_DIM)
     cfg = psa.EngineConfig(n_chains=total_chains, schedule=sched, precision=prec, seed=0)
@@ -220,8 +352,7 @@ def main():
     else:
         plan = psa.Plan(f, cfg, engine=2)
     levels = plan.levels
-    evals_per_step_local = chains_per_gpu * (1 + SCHEDULE[3] * levels)
-    evals_per_step = evals_per_step_local * world
+    evals_per_step = total_chains * (1 + SCHEDULE[3] * levels)
 
     stream = torch.cuda.current_stream()
     sh = stream.cuda_stream
@@ -322,10 +453,12 @@ def main():
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": scaling,
         "vs_baseline": None, "dtype": args.precision,
         "data": "synthetic (normalized Schwefel on [-512,512]^100, box-centre start, seed 0)",
-        "config": {"workload": "configs[1]: synchronous SA, normalized Schwefel n=100, 2^20 chains per GPU",
+        "config": {"workload": ("configs[4]: synchronous SA, normalized Schwefel n=100, "
+                                f"{total_chains} chains sharded over {world} GPU(s)") if args.chains_total > 0 else
+                               "configs[1]: synchronous SA, normalized Schwefel n=100, 2^20 chains per GPU",
                    "n": N_DIM, "chains_per_gpu": chains_per_gpu, "chains_total": total_chains,
                    "schedule": {"t0": SCHEDULE[0], "t_min": args.tmin, "rho": SCHEDULE[2],
                                 "sweep_length": SCHEDULE[3], "levels": levels},
@@ -380,6 +513,10 @@ def main():
         except Exception as e:  # pragma: no cover - reported, not fatal
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": None, "kind": "reference",
                                     "sample": f"unavailable: {e}"}
+    if rank == 0 and not args.no_cpu_baseline and "cpu_baseline" in line and line["cpu_baseline"]["value"]:
+        line["parity"] = parity_vs_reference(psa, f)
+    if world == 1 and not args.no_configs:
+        line["configs"] = measure_configs(psa, torch, flush)
     if rank == 0:
         print(json.dumps(line), flush=True)
     plan.close()

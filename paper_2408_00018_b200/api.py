@@ -611,7 +611,13 @@ class Plan:
                                                           e.ctypes.data_as(C.POINTER(C.c_double)), self.levels))
         return w, e
 
-    def close(self):
+    def close(self, _sync: bool = True):
+        # a multi-process shard waits for every rank before it unmaps the
+        # peers' mailboxes and frees its own (dist.make_sharded_plan)
+        hook = getattr(self, "_before_close", None)
+        if _sync and hook is not None and self._p:
+            self._before_close = None
+            hook()
         for ptr in getattr(self, "_opened", []):
             self._lib.psa_ipc_close(C.c_void_p(ptr))
         self._opened = []
@@ -621,7 +627,7 @@ class Plan:
 
     def __del__(self):
         try:
-            self.close()
+            self.close(_sync=False)
         except Exception:
             pass
 

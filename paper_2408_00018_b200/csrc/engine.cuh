@@ -663,6 +663,12 @@ PSA_HD bool better(const Cand& a, const Cand& b) {
 
 PSA_DEV Cand empty_cand() { return Cand{__longlong_as_double(0x7ff0000000000000ll), INT32_MAX, -1}; }
 
+constexpr double kInf = __builtin_huge_val();
+
+// A start-scan candidate (engines.cpp:161-167: `if (E[c] < best_f)` from
+// best_f = +inf): NaN and +inf energies never qualify.
+PSA_DEV Cand start_cand(double e, int32_t c) { return e < kInf ? Cand{e, c, 0} : empty_cand(); }
+
 PSA_DEV Cand shfl_cand(const Cand& v, int src_lane_xor) {
     Cand o;
     o.e = __shfl_xor_sync(0xffffffffu, v.e, src_lane_xor);

@@ -26,6 +26,8 @@
 
 #include <stdint.h>
 
+#include <type_traits>
+
 #include "engine.cuh"
 #include "engine_host.h"
 
@@ -472,7 +474,7 @@ __device__ __forceinline__ void v2_body(const EngineArgs& a) {
                         }
                         e = Cost::template energy<NT>(prow, n, a.family);
                         st.draws += static_cast<uint64_t>(n);
-                        const Cand s1{static_cast<double>(e), static_cast<int32_t>(c), 0};
+                        const Cand s1 = start_cand(static_cast<double>(e), static_cast<int32_t>(c));
                         if (better(s1, sbest)) sbest = s1;
                     }
                     ctr = static_cast<uint32_t>(n);
@@ -523,9 +525,9 @@ __device__ __forceinline__ void v2_body(const EngineArgs& a) {
                     PairOf<Cost>::template energy<NT>(prow, n, eA, eB);
                     ctr = static_cast<uint32_t>(n);
                     st.draws += static_cast<uint64_t>(n) * (vB ? 2 : 1);
-                    const Cand s1{static_cast<double>(eA), static_cast<int32_t>(cA), 0};
+                    const Cand s1 = start_cand(static_cast<double>(eA), static_cast<int32_t>(cA));
                     if (better(s1, sbest)) sbest = s1;
-                    const Cand s2{static_cast<double>(eB), static_cast<int32_t>(cB), 0};
+                    const Cand s2 = start_cand(static_cast<double>(eB), static_cast<int32_t>(cB));
                     if (vB && better(s2, sbest)) sbest = s2;
                 } else {
                     unsigned long long* u = reinterpret_cast<unsigned long long*>(prow);
@@ -558,7 +560,7 @@ __device__ __forceinline__ void v2_body(const EngineArgs& a) {
                 e = row_energy<Cost, NT>(row, n, a.family);
                 ctr = static_cast<uint32_t>(n);
                 st.draws += static_cast<uint64_t>(n);
-                const Cand s{static_cast<double>(e), static_cast<int32_t>(c), 0};
+                const Cand s = start_cand(static_cast<double>(e), static_cast<int32_t>(c));
                 if (better(s, sbest)) sbest = s;
             } else {
                 for (int k = 0; k < n * A; ++k) row[k] = vs[k];
@@ -592,28 +594,31 @@ __device__ __forceinline__ void v2_body(const EngineArgs& a) {
         w = block_argmin(w, scratch);
         if (l == 0 && a.random_start) ws = block_argmin(ws, scratch);
 
-        // level-0 best-so-far: the start scan (engines.cpp:161-167)
-        if (l == 0 && blockIdx.x == 0) {
-            if (a.random_start) {
-                for (int k = tid; k < n; k += B) a.best_x[k] = random_start_coord(a, box, ws.c, k);
-                if (tid == 0) { sh->best_f = ws.e; sh->best_c = ws.c; }
-            } else {
-                for (int k = tid; k < n; k += B) a.best_x[k] = xs[k];
-                if (tid == 0) { sh->best_f = sh->estar; sh->best_c = 0; }
-            }
-        }
         // the level's start point of the winner -> xs
         if (l == 0 && a.random_start)
             for (int k = tid; k < n; k += B) xs[k] = random_start_coord(a, box, w.c, k);
         __syncthreads();
         replay_winner(a, box, xs, l, w.c, masks);
         __syncthreads();
-        if (a.world > 1) exchange_level(a, xs, w, ws, l, scratch); // the multi-GPU minloc
+        if (a.world > 1) exchange_level(a, xs, w, ws, l, scratch); // the multi-GPU minloc (w, ws global)
+        // level-0 best-so-far: the start scan of engines.cpp:161-167 — a strict
+        // `<` against +inf in chain order, so NaN and +inf starts never count
+        // (start_cand); with no qualifying start best_f stays +inf, the chain
+        // 0 and best_x NaN (the reference leaves best_x empty)
+        if (l == 0 && blockIdx.x == 0) {
+            const bool have = a.random_start ? ws.c != INT32_MAX : sh->estar < kInf;
+            for (int k = tid; k < n; k += B)
+                a.best_x[k] = !have ? __longlong_as_double(0x7ff8000000000000ll)
+                              : a.random_start ? random_start_coord(a, box, ws.c, k) : a.start[k];
+            __syncthreads(); // every thread has read sh->estar
+            if (tid == 0 && have) {
+                sh->best_f = a.random_start ? ws.e : sh->estar;
+                sh->best_c = a.random_start ? ws.c : 0;
+            }
+        }
         cache_point<R, Cost>(xs, vs, n, a.family);
         __syncthreads();
-        if (tid == 0) {
-            sh->estar = w.e;
-            }
+        if (tid == 0) sh->estar = w.e;
         __syncthreads();
         if (blockIdx.x == 0) {
             const bool improve = w.e < sh->best_f; // engines.cpp:193 (strict)
@@ -1220,6 +1225,10 @@ EngineKernels sep_kernels(int n) {
     case 10: return KernelSet<R, SepCost<R, F>, 10>::get();
     case 30: return KernelSet<R, SepCost<R, F>, 30>::get();
     case 100: return KernelSet<R, SepCost<R, F>, 100>::get();
+    // configs[3] (the hybrid's SA phase) runs normalized Schwefel at n = 500
+    case 500:
+        if constexpr (std::is_same<F<R>, Schwefel<R>>::value) return KernelSet<R, SepCost<R, F>, 500>::get();
+        else return KernelSet<R, SepCost<R, F>>::get();
     default: return KernelSet<R, SepCost<R, F>>::get();
     }
 }

@@ -31,6 +31,7 @@
 #include <cuda_runtime.h>
 
 #include <stdint.h>
+#include <stdio.h>
 
 #include "engine.cuh"
 #include "engine_host.h"
@@ -125,6 +126,31 @@ __global__ void __launch_bounds__(512) nm_kernel(const NMArgs a) {
     int* ord_s = reinterpret_cast<int*>(D + (n + 1));       // n+1 sorted order
     int* ist = ord_s + (n + 1);                             // int scalars: [0] vp, [1] D owner (-1 = stale)
     unsigned long long evals = 0;
+#ifdef PSA_NM_PROFILE
+    // measurement builds only (scripts/build_nm_profile.sh): cycles per phase
+    // and path counters on CTA 0 thread 0, printed at the end
+    unsigned long long pf[6] = {0, 0, 0, 0, 0, 0}, pc[6] = {0, 0, 0, 0, 0, 0};
+    long long tq = clock64();
+#define NMP(i)                                   \
+    do {                                         \
+        if (rank == 0 && tid == 0) {             \
+            const long long t_ = clock64();      \
+            pf[i] += static_cast<unsigned long long>(t_ - tq); \
+            tq = t_;                             \
+        }                                        \
+    } while (0)
+#define NMC(i, v)                                \
+    do {                                         \
+        if (rank == 0 && tid == 0) pc[i] += (v); \
+    } while (0)
+#else
+#define NMP(i) \
+    do {       \
+    } while (0)
+#define NMC(i, v) \
+    do {          \
+    } while (0)
+#endif
     double* X = a.X;
     // Q (and the centroid checkpoints P) of this CTA's columns: in shared
     // memory when the slice fits (a.q_smem), else in global memory.  Element
@@ -253,7 +279,11 @@ __global__ void __launch_bounds__(512) nm_kernel(const NMArgs a) {
     // the introsort's disjoint ranges one per lane, level by level; the same
     // order as sort(), see parsa_stdsort_pairs.hpp); with NaNs thread 0 runs
     // sort() itself.  Range lists: rk / saved (idle here), 3 ints per range.
-    auto exact_sort = [&]() {
+    //  w >= 0: the sort follows replace_worst(w), the only vertex that changed:
+    //  centroid prefixes before the first reordered position and (if the best
+    //  vertex stays) every other diameter stay valid; w < 0: all are stale.
+    auto exact_sort = [&](int w) {
+        if (tid == 0) ist[3] = n + 1;
         int has_nan = 0;
         for (int p = tid; p <= n; p += B) {
             const double fk = f_s[ord_s[p]];
@@ -268,15 +298,35 @@ __global__ void __launch_bounds__(512) nm_kernel(const NMArgs a) {
         } else if (tid < 32) {
             exact_sort_tasks(kp, n + 1, rk, saved, &ist[2]);
         }
-        if (tid == 0) {
-            ist[0] = 0;
-            ist[1] = -1;
-        }
+        __syncthreads();
+        const int old_best = ord_s[0];
+        for (int p = tid; p <= n; p += B)
+            if (kp[p].id != ord_s[p]) atomicMin(&ist[3], p); // first reordered position
         __syncthreads();
         for (int p = tid; p <= n; p += B) ord_s[p] = kp[p].id;
         __syncthreads();
+        const bool keep_d = w >= 0 && ist[1] >= 0 && ord_s[0] == old_best;
+        __syncthreads(); // every thread has read ist[1] before thread 0 updates it
+        NMC(0, 1);
+        NMC(4, keep_d ? 1 : 0);
+        if (tid == 0) {
+            ist[0] = w >= 0 ? min(ist[0], ist[3]) : 0;
+            if (!keep_d) ist[1] = -1;
+        }
+        __syncthreads();
+        if (keep_d) vertex_diameter(w, ord_s[0]);
+        __syncthreads();
     };
     auto full_sort = [&]() {
+        // a NaN value breaks the rank count below (it would share rank 0 with
+        // the minimum and leave positions unwritten): such keys go straight to
+        // the exact introsort, whose one-thread form handles them
+        int nan_key = 0;
+        for (int v = tid; v <= n; v += B) nan_key |= f_s[v] != f_s[v];
+        if (__syncthreads_or(nan_key)) {
+            exact_sort(-1);
+            return;
+        }
         for (int p = tid; p <= n; p += B) saved[p] = ord_s[p];
         __syncthreads();
         // rank of the vertex at position p = #{q : f_q < f_p or (f_q == f_p and q < p)}
@@ -297,7 +347,7 @@ __global__ void __launch_bounds__(512) nm_kernel(const NMArgs a) {
         if (__syncthreads_or(tie)) {
             for (int p = tid; p <= n; p += B) ord_s[p] = saved[p];
             __syncthreads();
-            exact_sort();
+            exact_sort(-1);
         }
         if (tid == 0) {
             ist[0] = 0;
@@ -320,7 +370,7 @@ __global__ void __launch_bounds__(512) nm_kernel(const NMArgs a) {
             if (p + 1 < n) tie |= equiv(f_s[ord_s[p]], f_s[ord_s[p + 1]]);
         }
         if (__syncthreads_or(tie)) {
-            exact_sort();
+            exact_sort(w);
             return;
         }
         // distinct values: the new vertex lands after every smaller value
@@ -351,6 +401,7 @@ __global__ void __launch_bounds__(512) nm_kernel(const NMArgs a) {
         // termination (nelder_mead.cpp:67-68; simplex_diameter :21-27)
         const int b0 = ord_s[0];
         if (ist[1] != b0) {
+            NMC(1, 1);
             // all diameters (own columns) against the best: one warp per vertex
             const int lane = tid & 31, warp = tid >> 5, nw = B >> 5;
             for (int v = warp; v <= n; v += nw) {
@@ -378,11 +429,13 @@ __global__ void __launch_bounds__(512) nm_kernel(const NMArgs a) {
         double dmax = 0;
         for (int r = 0; r < CL; ++r) dmax = dmax < dslot[r] ? dslot[r] : dmax;
         if (f_s[ord_s[n]] - f_s[ord_s[0]] <= a.f_tol || dmax <= a.x_tol) break;
+        NMP(0);
 
         // centroid of the n best (nelder_mead.cpp:70-73), own columns: re-add
         // from the checkpoint at or below the first changed position (prefix
         // sums are stored every kNmCheckpoint positions)
         const int vp = (ist[0] / kNmCheckpoint) * kNmCheckpoint;
+        NMC(2, n - vp);
         for (int j = tid; j < nc; j += B) {
             double c = Pb[static_cast<size_t>(vp / kNmCheckpoint) * qst + j];
             // one checkpoint segment at a time: its (up to 16) quotients are
@@ -410,14 +463,17 @@ __global__ void __launch_bounds__(512) nm_kernel(const NMArgs a) {
             xr[j] = clampd(cen[j] + a.reflect * (cen[j] - col(worst, j)), a.lower[k], a.upper[k]);
         }
         __syncthreads();
+        NMP(1);
         const double fr = eval(xr);
         ++evals;
+        NMP(2);
         if (fr < f_s[ord_s[0]]) {
             for (int j = tid; j < nc; j += B)
                 xe[j] = clampd(cen[j] + a.expand * (xr[j] - cen[j]), a.lower[c0 + j], a.upper[c0 + j]);
             __syncthreads();
             const double fe = eval(xe);
             ++evals;
+            NMP(2);
             if (fe < fr) replace_worst(xe, fe);
             else replace_worst(xr, fr);
         } else if (fr < f_s[ord_s[n - 1]]) {
@@ -431,6 +487,7 @@ __global__ void __launch_bounds__(512) nm_kernel(const NMArgs a) {
             __syncthreads();
             const double fc = eval(xc);
             ++evals;
+            NMP(2);
             if (fc < (outside ? fr : worst_f)) {
                 replace_worst(xc, fc);
             } else {
@@ -450,10 +507,19 @@ __global__ void __launch_bounds__(512) nm_kernel(const NMArgs a) {
                 eval_rows(1, n, ord_s);
                 evals += n;
                 full_sort();
+                NMC(3, 1);
+                NMP(4);
             }
         }
+        NMP(3);
         __syncthreads();
     }
+#ifdef PSA_NM_PROFILE
+    if (rank == 0 && tid == 0)
+        printf("NMPROF iters=%d evals=%llu cyc_term=%llu cyc_centroid=%llu cyc_eval=%llu cyc_replace=%llu "
+               "cyc_shrink=%llu tie_sorts=%llu diam_full=%llu readd_len=%llu shrinks=%llu keep_d=%llu\n",
+               iter, evals, pf[0], pf[1], pf[2], pf[3], pf[4], pc[0], pc[1], pc[2], pc[3], pc[4]);
+#endif
     const int b = ord_s[0];
     for (int j = tid; j < nc; j += B) a.x_best[c0 + j] = col(b, j);
     if (rank == 0 && tid == 0) {

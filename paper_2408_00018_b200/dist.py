@@ -59,6 +59,7 @@ def make_sharded_plan(f: ObjectiveFunction, cfg: EngineConfig, group=None, max_b
         peers = [plan.mailbox() if r == rank else plan.open_ipc(handles[r]) for r in range(world)]
         plan.set_peers(peers)
         dist.barrier(group)
+        plan._before_close = lambda: dist.barrier(group)
     return plan
 
 
