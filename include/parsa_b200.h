@@ -247,6 +247,10 @@ psa_status psa_plan_set_peers(psa_plan* p, void* const* mailboxes, int32_t world
  * engines.cpp:187-192), copied to caller buffers of `capacity` entries */
 psa_status psa_plan_level_detail(const psa_plan* p, int32_t* winners, double* winner_f,
                                  int32_t capacity);
+/* deferred-fold plans (v2_lazy_kernel): how many trials of the last fetched
+ * run needed an exact fold to settle their Metropolis decision (0 for the
+ * other kernels, which fold every trial) */
+psa_status psa_plan_stats(const psa_plan* p, uint64_t* exact_settles);
 
 /* ---- device probes for parity tests ------------------------------------
  * Run the device implementations of the RNG and the cost functions on

@@ -611,6 +611,13 @@ class Plan:
                                                           e.ctypes.data_as(C.POINTER(C.c_double)), self.levels))
         return w, e
 
+    def exact_settles(self) -> int:
+        """Deferred-fold plans: trials of the last fetched run whose decision
+        needed exact folds (psa_plan_stats)."""
+        v = C.c_uint64()
+        _raise(self._lib, self._lib.psa_plan_stats(self._p, C.byref(v)))
+        return v.value
+
     def close(self, _sync: bool = True):
         # a multi-process shard waits for every rank before it unmaps the
         # peers' mailboxes and frees its own (dist.make_sharded_plan)

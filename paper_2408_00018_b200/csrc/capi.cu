@@ -255,6 +255,8 @@ struct psa_plan {
     bool hbm_rows = false;        // chain rows in HBM (large n) instead of shared memory
     bool pair = false;            // two chains per thread (v2_pair_kernel)
     bool pc = false;              // producer/consumer blocks (v2_pc_kernel)
+    bool lazy = false;            // deferred fold (v2_lazy_kernel)
+    uint64_t last_settles = 0;    // exact-fold decisions of the last fetched run
     size_t mask_stride = 0;
     const void* kernel = nullptr; // the engine kernel this plan launches
     DevBuf<double> d_lower, d_width, d_start, d_temps, d_trace, d_bestx, d_xbest, d_winner_f, d_xrows;
@@ -321,10 +323,22 @@ void plan_build(psa_plan* p, const psa_objective* f, const psa_engine_config* cf
     const DeviceLimits& lim = device_limits(dev);
     const size_t smem_cap = lim.smem_optin;
     auto smem_of = [&](int B) { return engine == 1 ? p->ks.smem_v1(n, B, !uniform) : p->ks.smem_v2(n, B, !uniform); };
+    // Kernel choice (all variants are bit-identical; PSA_V2_MODE = single |
+    // pair | pc | lazy forces one for A/B measurements, PSA_LAZY=0 turns the
+    // deferred fold off).
+    const char* mode_env = std::getenv("PSA_V2_MODE");
+    const std::string mode = mode_env ? mode_env : "";
+    const char* lazy_env = std::getenv("PSA_LAZY");
+    // Affine families (LazyOf): the deferred-fold sweep settles decisions
+    // from an energy interval and folds only when the interval straddles the
+    // Metropolis threshold (engine.cuh) — no n-term fold per trial.
+    p->lazy = engine == 2 && p->ks.v2z && !(lazy_env && lazy_env[0] == '0') &&
+              (mode.empty() || mode == "lazy");
     // block size: of 128/96/64/32 threads, the one that keeps the most
     // chain rows resident per SM (large rows: three 32-thread blocks hold
     // more rows than one 64-thread block); ties go to the larger block
     auto kern_of = [&](bool g) {
+        if (p->lazy) return g ? p->ks.v2gz : p->ks.v2z;
         return engine == 1 ? (g ? p->ks.v1g : p->ks.v1) : (g ? p->ks.v2g : p->ks.v2);
     };
     int B = 32;
@@ -357,11 +371,7 @@ void plan_build(psa_plan* p, const psa_objective* f, const psa_engine_config* cf
     }
     p->block = B;
     p->smem = p->hbm_rows ? p->ks.smem_g(n, B, !uniform) : smem_of(B);
-    const void* kern = engine == 1 ? (p->hbm_rows ? p->ks.v1g : p->ks.v1) : (p->hbm_rows ? p->ks.v2g : p->ks.v2);
-    // Kernel choice (all variants are bit-identical; PSA_V2_MODE = single |
-    // pair | pc forces one for A/B measurements).
-    const char* mode_env = std::getenv("PSA_V2_MODE");
-    const std::string mode = mode_env ? mode_env : "";
+    const void* kern = kern_of(p->hbm_rows);
     // Few chains (fewer than 8 warps per SM of one chain per thread): each
     // chain's level is a latency-bound dependency chain, so producer warps
     // take the proposals off its critical path (v2_pc_kernel).
@@ -373,7 +383,7 @@ void plan_build(psa_plan* p, const psa_objective* f, const psa_engine_config* cf
     const bool few = static_cast<long long>(p->chains_local) < 256ll * lim.sms && !heavy_finish;
     const void* pc_kern = engine == 2 ? p->ks.v2pc : p->ks.v1pc;
     const size_t smem_pc = engine == 2 ? p->ks.smem_v2pc(n, 128, !uniform) : p->ks.smem_v1pc(n, 128, !uniform);
-    if (!p->hbm_rows && pc_kern && (mode == "pc" || (mode.empty() && few)) && smem_pc <= smem_cap) {
+    if (!p->lazy && !p->hbm_rows && pc_kern && (mode == "pc" || (mode.empty() && few)) && smem_pc <= smem_cap) {
         p->pc = true;
         p->block = B = 128;
         p->smem = smem_pc;
@@ -385,7 +395,7 @@ void plan_build(psa_plan* p, const psa_objective* f, const psa_engine_config* cf
     // enough pairs to fill them (small chain counts or large n keep one chain
     // per thread; PSA_V2_MODE=pair forces pairs whenever the rows fit).
     const void* pair_kern = engine == 2 ? p->ks.v2p : p->ks.v1p;
-    if (!p->pc && !p->hbm_rows && pair_kern && mode != "single" && mode != "pc") {
+    if (!p->lazy && !p->pc && !p->hbm_rows && pair_kern && mode != "single" && mode != "pc") {
         int Bp = 128;
         while (Bp > 32 && p->ks.smem_v2p(n, Bp, !uniform) > smem_cap) Bp /= 2;
         const size_t smem_p = p->ks.smem_v2p(n, Bp, !uniform);
@@ -487,6 +497,13 @@ void plan_build(psa_plan* p, const psa_objective* f, const psa_engine_config* cf
     a.world = p->world;
     a.rank = p->rank;
     a.spin_limit = 60ll * 2000000000ll; // ~60 s at 2 GHz
+    if (p->lazy) {
+        std::vector<double> upper(n);
+        for (int k = 0; k < n; ++k) upper[k] = f->lower[k] + width[k];
+        // S is re-summed from V* at every level start: at most N updates
+        a.lazy_r = p->ks.lazy_radius(n, p->N, f->lower, upper.data());
+        a.lazy_alpha = p->ks.lazy_alpha_of(n);
+    }
     if (p->world > 1) {
         p->rec_stride = (48 + sizeof(double) * static_cast<size_t>(n) + 127) & ~size_t(127);
         p->d_mail.alloc(2 * static_cast<size_t>(p->world) * p->rec_stride);
@@ -551,6 +568,7 @@ void plan_fetch(psa_plan* p, cudaStream_t s, psa_run_result* out) {
         m << "rng draw count mismatch: engine reported " << o.rng_draws << ", expected " << p->expected_draws;
         fail(PSA_ERR_LOGIC, m.str());
     }
+    p->last_settles = o.exact_settles;
     out->best_f = o.best_f;
     out->winning_chain = o.best_chain;
     out->evaluations = o.evaluations;
@@ -954,6 +972,8 @@ psa_status psa_plan_describe(const psa_plan* p, char* buf, int32_t capacity) {
                                                              : "v1_kernel (shared-memory rows)")
                              : p->pair     ? "v2_pair_kernel (two chains per thread, shared-memory pair rows)"
                              : p->pc       ? "v2_pc_kernel (producer/consumer warps, 32 chains per block)"
+                             : p->lazy     ? (p->hbm_rows ? "v2_lazy_kernel (deferred fold, HBM SoA rows)"
+                                                              : "v2_lazy_kernel (deferred fold, one chain per thread, shared-memory rows)")
                              : p->hbm_rows ? "v2_kernel (HBM SoA rows)"
                                            : "v2_kernel (one chain per thread, shared-memory rows)";
         d << layout << " precision=" << (p->precision == PSA_F32 ? "f32" : "f64") << " family=" << p->family
@@ -971,6 +991,13 @@ psa_status psa_plan_level_detail(const psa_plan* p, int32_t* winners, double* wi
         const int m = std::min(capacity, p->levels);
         if (winners) cuda_check(cudaMemcpy(winners, p->d_winner.p, sizeof(int32_t) * m, cudaMemcpyDeviceToHost), "D2H");
         if (winner_f) cuda_check(cudaMemcpy(winner_f, p->d_winner_f.p, sizeof(double) * m, cudaMemcpyDeviceToHost), "D2H");
+    });
+}
+
+psa_status psa_plan_stats(const psa_plan* p, uint64_t* exact_settles) {
+    return guarded([&] {
+        if (!p || !exact_settles) fail(PSA_ERR_INVALID_ARGUMENT, "parsa_b200: null argument");
+        *exact_settles = p->last_settles;
     });
 }
 

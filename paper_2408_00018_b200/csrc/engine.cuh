@@ -342,6 +342,7 @@ struct Box {
 struct SweepStats {
     uint64_t evals;
     uint64_t draws;
+    uint64_t settles = 0; // deferred fold: decisions settled by exact folds
 };
 
 // row: this thread's 16-byte aligned shared-memory state row (Row = R*), or
@@ -449,6 +450,186 @@ PSA_DEV R sweep(Row row, int n_rt, int family, R E, double temperature, uint32_t
     st.evals += static_cast<uint64_t>(N);
     st.draws += 3ull * static_cast<uint64_t>(N);
     return E;
+}
+
+// ---------------------------------------------------------------------------
+// Deferred fold: Metropolis decisions from an energy interval
+//
+// For the affine families of objectives.cuh (LazyOf: E = finish(s), s one
+// additive fold of the cached terms) a trial's exact energy is only needed
+// when its decision depends on the last bits.  The sweep tracks, per chain,
+//   S  = init + sigma * sum_k t_k   in double (one add per accepted move),
+// and knows a radius rE (host-computed, lazy_radius below) such that the
+// exact binary32/binary64 energy the reference computes — the fold in index
+// order, then finish — lies in [alpha*S - rE, alpha*S + rE]:
+//   * fold rounding: each of the n adds rounds by at most u|partial|, and
+//     |partial_k| <= |init| + sum_{j<=k} |t_j|, so the fold is within
+//     u(1+nu) (n|init| + sum_k (n-k) Tmax_k) of the exact sum (Tmax_k bounds
+//     |t_k| over the box, LazyOf::term_bound);
+//   * the double tracking of S adds at most 2^-53 (|init| + sum Tmax) per
+//     add (n adds at the level start, two per update);
+//   * finish rounds fin_round times (u relative), the double arithmetic of
+//     the centre and the interval ends adds 2^-48 of the largest energy.
+// The old energy is either exact (after a fold: radius 0) or such an
+// interval.  With d in [lo, hi] the decision of sa_core.cpp:46-55 is certain
+// when hi <= 0 or x(hi) < band.lo (accept: every d in the interval accepts,
+// x is monotone in d) or when lo > 0 and x(lo) > band.hi (reject) — the same
+// log-domain band as metropolis_fast, whose margin already covers the
+// rounding of x.  Otherwise (a warp-uniform rare branch) the old state and
+// the trial are folded exactly and metropolis_fast / Accept::exact decide as
+// in sweep().  Decisions are therefore identical to the reference's, and the
+// energies that leave the sweep (its end energy, every energy compared in a
+// settled decision) are the exact folds.  An accepted move writes its term to
+// the row; a rejected one touches nothing.  NaN/inf anywhere makes every
+// comparison false, i.e. the exact path.
+// ---------------------------------------------------------------------------
+
+// S of a row: init, then sigma * t_k in index order (double)
+template <class Fam, class Row>
+PSA_DEV double lazy_sum(const Row& row, int n) {
+    using L = LazyOf<Fam>;
+    double s = static_cast<double>(Fam::init(0, n));
+    for (int k = 0; k < n; ++k) {
+        const double t = static_cast<double>(row[k]);
+        s = L::sigma > 0 ? s + t : s - t;
+    }
+    return s;
+}
+
+// the radius rE of the interval (host); updates = moves applied to S since
+// it was last summed from a row
+template <class R, template <class> class F>
+double lazy_radius(int n, long long updates, const double* lower, const double* upper) {
+    using Fam = F<R>;
+    using L = LazyOf<Fam>;
+    const double u = sizeof(R) == 4 ? 0x1.0p-24 : 0x1.0p-53;
+    const double init = fabs(static_cast<double>(Fam::init(0, n)));
+    double tsum = 0, wmax = 0, tmax = 0;
+    for (int k = 0; k < n; ++k) {
+        const double t = L::term_bound(lower[k], upper[k]) * (1.0 + 0x1.0p-16);
+        tsum += t;
+        wmax += static_cast<double>(n - k) * t;
+        tmax = fmax(tmax, t);
+    }
+    const double P = init + tsum;                  // bounds |S| and every partial sum
+    const double a = fabs(L::alpha(n));
+    const double fold = u * (1.0 + 2.0 * n * u) * (static_cast<double>(n) * init + wmax);
+    const double eta = 0x1.0p-53 * (static_cast<double>(n) * P + static_cast<double>(updates + 1) * (2.0 * tmax + P));
+    const double cmax = a * P;
+    const double r = a * (fold + eta) + L::fin_round * u * cmax + 0x1.0p-48 * cmax;
+    return r * 1.01;
+}
+
+template <class R, class Cost, int NT = 0, class Row = R*>
+PSA_DEV R sweep_lazy(Row row, int n_rt, int family, R E, double S, double temperature, uint32_t chain,
+                     uint32_t level, uint32_t ctr, int N, const Box& box, const PhiloxKeys& keys,
+                     uint32_t* mask, size_t mask_stride, double* x, size_t x_stride, SweepStats& st,
+                     double rE, double alpha) {
+    using L = LazyOf<typename Cost::Fam>;
+    static_assert(Cost::A == 1, "deferred fold: one accumulator");
+    const int n = NT > 0 ? NT : n_rt;
+    const float k2 = metropolis_k2(temperature);
+    const PhiloxChain pc = philox_chain(chain, level, keys);
+    const double idx_scale = static_cast<double>(n) * 0x1.0p-53;
+    double co = static_cast<double>(E); // old energy in [co - ro, co + ro]; ro == 0: exact
+    double ro = 0.0;
+    int d;
+    double xnew;
+    R tn[1];
+    uint64_t m3;
+    uint64_t q1, q2, q3;
+    {
+        const uint64_t m1 = draw_bits53_fast(ctr, pc, keys);
+        const uint64_t m2 = draw_bits53_fast(ctr + 1, pc, keys);
+        m3 = draw_bits53_fast(ctr + 2, pc, keys);
+        d = min(static_cast<int>(static_cast<double>(m1) * idx_scale), n - 1);
+        xnew = box.point(d, bits_to_uniform(m2));
+        Cost::cache(static_cast<R>(xnew), d, n, tn);
+        q1 = draw_bits53_fast(ctr + 3, pc, keys);
+        q2 = draw_bits53_fast(ctr + 4, pc, keys);
+        q3 = draw_bits53_fast(ctr + 5, pc, keys);
+    }
+    for (int j0 = 0; j0 < N; j0 += 32) {
+        const int jn = N - j0 < 32 ? N - j0 : 32;
+        uint32_t word = 0;
+        for (int j = 0; j < jn; ++j) {
+            const R to = row[d];
+            const int dn = min(static_cast<int>(static_cast<double>(q1) * idx_scale), n - 1);
+            const double xn = box.point(dn, bits_to_uniform(q2));
+            R tnn[1];
+            bool ok;
+            Cost::cache_common(static_cast<R>(xn), dn, n, tnn, ok);
+            const uint64_t r1 = draw_bits53_fast(ctr + 6, pc, keys);
+            const uint64_t r2 = draw_bits53_fast(ctr + 7, pc, keys);
+            const uint64_t r3 = draw_bits53_fast(ctr + 8, pc, keys);
+            const MBand b3 = metropolis_band(m3);
+            // the interval decision
+            const double dl = static_cast<double>(tn[0]) - static_cast<double>(to);
+            const double St = L::sigma > 0 ? S + dl : S - dl;
+            const double ct = alpha * St;
+            const double dh = ct - co, rr = rE + ro;
+            const double hi = dh + rr, lo = dh - rr;
+            const float xh = static_cast<float>(hi) * k2, xl = static_cast<float>(lo) * k2;
+            int r = ((hi <= 0.0) | (xh < b3.lo)) ? 1 : (((lo > 0.0) & (xl > b3.hi)) ? 0 : -1);
+            if (__any_sync(__activemask(), !ok))
+                if (!ok) Cost::cache(static_cast<R>(xn), dn, n, tnn);
+            bool settled = false;
+            if (__any_sync(__activemask(), r < 0)) {
+                // rare: fold exactly (the whole warp folds; every lane with an
+                // interval energy takes the exact old value for free)
+                if (__any_sync(__activemask(), (r < 0) & (ro != 0.0))) {
+                    const R eo = row_energy<Cost, NT>(row, n, family);
+                    if (ro != 0.0) {
+                        co = static_cast<double>(eo);
+                        ro = 0.0;
+                    }
+                }
+                if (r < 0) row[d] = tn[0];
+                const R et = row_energy<Cost, NT>(row, n, family);
+                if (r < 0) {
+                    int q = metropolis_fast<R>(et, static_cast<R>(co), k2, b3);
+                    if (q < 0) q = Accept<R>::exact(static_cast<double>(et) - co, temperature, m3);
+                    if (q) {
+                        co = static_cast<double>(et);
+                        ro = 0.0;
+                        S = St;
+                    } else {
+                        row[d] = to;
+                    }
+                    r = q;
+                    settled = true;
+                    st.settles += 1;
+                }
+            }
+            if (r && !settled) {
+                row[d] = tn[0];
+                S = St;
+                co = ct;
+                ro = rE;
+            }
+            ctr += 3;
+            if (r) {
+                word |= 1u << j;
+                if (x) x[static_cast<size_t>(d) * x_stride] = xnew;
+            }
+            d = dn;
+            xnew = xn;
+            m3 = q3;
+            q1 = r1;
+            q2 = r2;
+            q3 = r3;
+            tn[0] = tnn[0];
+        }
+        if (mask) mask[static_cast<size_t>(j0 >> 5) * mask_stride] = word;
+    }
+    // the end energy is the exact fold
+    if (__any_sync(__activemask(), ro != 0.0)) {
+        const R e = row_energy<Cost, NT>(row, n, family);
+        if (ro != 0.0) co = static_cast<double>(e);
+    }
+    st.evals += static_cast<uint64_t>(N);
+    st.draws += 3ull * static_cast<uint64_t>(N);
+    return static_cast<R>(co);
 }
 
 // ---------------------------------------------------------------------------

@@ -23,6 +23,7 @@ struct OutScalars {
     int32_t pad;
     unsigned long long evaluations;
     unsigned long long rng_draws;
+    unsigned long long exact_settles; // deferred fold: trials decided by exact folds
 };
 
 // Kernel arguments (passed by value; all pointers are device pointers).
@@ -65,6 +66,9 @@ struct EngineArgs {
     char* const* mail_peers; // device array: every GPU's mailbox as seen from here
     long long spin_limit;   // clock64 cycles before a missing peer is reported
     int* error_flag;
+    // deferred fold (v2_lazy_kernel): energy radius and finish slope
+    double lazy_r;
+    double lazy_alpha;
 };
 
 struct NMOut {
@@ -136,6 +140,11 @@ struct EngineKernels {
     size_t (*smem_v2)(int n, int B, bool box);
     size_t (*smem_v1)(int n, int B, bool box);
     size_t (*smem_eval)(int n, int B);
+    // deferred fold (LazyOf families), else nullptr
+    const void* v2z;  // shared-memory rows
+    const void* v2gz; // HBM rows
+    double (*lazy_radius)(int n, long long updates, const double* lower, const double* upper);
+    double (*lazy_alpha_of)(int n);
 };
 
 EngineKernels engine_kernels(int precision, int family, int n);

@@ -80,6 +80,7 @@ size_t engine_smem_bytes(int n, int B, bool box, bool rows_in_smem, bool pair = 
 
 struct SharedScalars {
     double estar;
+    double sstar; // deferred fold: S of the level start (lazy_sum of V*)
     double best_f;
     int32_t best_c;
     int32_t pad;
@@ -405,7 +406,8 @@ struct PairOf<SepCost<float, F>> {
     }
 };
 
-template <class R, class Cost, int NT, bool G, bool PAIR, bool PC = false>
+// LZ: the deferred-fold sweep (sweep_lazy; Cost = SepCost of a LazyOf family)
+template <class R, class Cost, int NT, bool G, bool PAIR, bool PC = false, bool LZ = false>
 __device__ __forceinline__ void v2_body(const EngineArgs& a) {
     constexpr int A = Cost::A;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -433,6 +435,7 @@ __device__ __forceinline__ void v2_body(const EngineArgs& a) {
     __syncthreads();
     if (tid == 0) {
         sh->estar = static_cast<double>(Cost::template energy<NT>(vs, n, a.family));
+        if constexpr (LZ) sh->sstar = lazy_sum<typename Cost::Fam>(vs, n);
         sh->best_f = __longlong_as_double(0x7ff0000000000000ll);
         sh->best_c = 0;
     }
@@ -567,8 +570,15 @@ __device__ __forceinline__ void v2_body(const EngineArgs& a) {
                 e = estar;
             }
             if (l == 0) st.evals += 1; // the start evaluation (engines.cpp:157)
-            e = sweep<R, Cost, NT>(row, n, a.family, e, temperature, c, static_cast<uint32_t>(l), ctr,
-                                   a.N, box, a.keys, masks + cl, a.mask_stride, nullptr, 0, st);
+            if constexpr (LZ) {
+                const double s0 = (l == 0 && a.random_start) ? lazy_sum<typename Cost::Fam>(row, n) : sh->sstar;
+                e = sweep_lazy<R, Cost, NT>(row, n, a.family, e, s0, temperature, c, static_cast<uint32_t>(l), ctr,
+                                            a.N, box, a.keys, masks + cl, a.mask_stride, nullptr, 0, st, a.lazy_r,
+                                            a.lazy_alpha);
+            } else {
+                e = sweep<R, Cost, NT>(row, n, a.family, e, temperature, c, static_cast<uint32_t>(l), ctr,
+                                       a.N, box, a.keys, masks + cl, a.mask_stride, nullptr, 0, st);
+            }
             const Cand mine{static_cast<double>(e), static_cast<int32_t>(c), 0};
             if (better(mine, best)) best = mine;
         }
@@ -618,7 +628,10 @@ __device__ __forceinline__ void v2_body(const EngineArgs& a) {
         }
         cache_point<R, Cost>(xs, vs, n, a.family);
         __syncthreads();
-        if (tid == 0) sh->estar = w.e;
+        if (tid == 0) {
+            sh->estar = w.e;
+            if constexpr (LZ) sh->sstar = lazy_sum<typename Cost::Fam>(vs, n);
+        }
         __syncthreads();
         if (blockIdx.x == 0) {
             const bool improve = w.e < sh->best_f; // engines.cpp:193 (strict)
@@ -642,21 +655,29 @@ __device__ __forceinline__ void v2_body(const EngineArgs& a) {
         a.out_scalars->best_chain = sh->best_c;
     }
     // accounting: device-side totals of evaluations and draws
-    __shared__ unsigned long long red_e, red_d;
-    if (tid == 0) { red_e = 0; red_d = 0; }
+    __shared__ unsigned long long red_e, red_d, red_s;
+    if (tid == 0) { red_e = 0; red_d = 0; red_s = 0; }
     __syncthreads();
     atomicAdd(&red_e, static_cast<unsigned long long>(st.evals));
     atomicAdd(&red_d, static_cast<unsigned long long>(st.draws));
+    if (LZ) atomicAdd(&red_s, static_cast<unsigned long long>(st.settles));
     __syncthreads();
     if (tid == 0) {
         atomicAdd(&a.out_scalars->evaluations, red_e);
         atomicAdd(&a.out_scalars->rng_draws, red_d);
+        if (LZ) atomicAdd(&a.out_scalars->exact_settles, red_s);
     }
 }
 
 template <class R, class Cost, int NT, bool G>
 __global__ void __launch_bounds__(PSA_V2_MAX_THREADS, PSA_V2_MIN_BLOCKS) v2_kernel(const EngineArgs a) {
     v2_body<R, Cost, NT, G, false>(a);
+}
+
+// deferred fold (sweep_lazy): one chain per thread, rows in shared memory or HBM
+template <class R, class Cost, int NT, bool G>
+__global__ void __launch_bounds__(PSA_V2_MAX_THREADS, PSA_V2_MIN_BLOCKS) v2_lazy_kernel(const EngineArgs a) {
+    v2_body<R, Cost, NT, G, false, false, true>(a);
 }
 
 // producer/consumer blocks for small chain counts: warp 0 consumes, warps
@@ -1180,6 +1201,24 @@ __global__ void sweep_one(const EngineArgs a, double* x, R* row, double* energy,
 // Host-side dispatch over (precision, family)
 // ---------------------------------------------------------------------------
 
+// deferred-fold capability of a cost (SepCost of a LazyOf family)
+template <class Cost>
+struct LazyCost {
+    static constexpr bool value = false;
+};
+template <class R, template <class> class F>
+struct LazyCost<SepCost<R, F>> {
+    static constexpr bool value = LazyOf<F<R>>::value;
+    static double radius(int n, long long updates, const double* lo, const double* hi) {
+        if constexpr (LazyOf<F<R>>::value) return lazy_radius<R, F>(n, updates, lo, hi);
+        else return -1.0;
+    }
+    static double alpha(int n) {
+        if constexpr (LazyOf<F<R>>::value) return LazyOf<F<R>>::alpha(n);
+        else return 0.0;
+    }
+};
+
 template <class R, class Cost, int NT = 0>
 struct KernelSet {
     static EngineKernels get() {
@@ -1202,6 +1241,16 @@ struct KernelSet {
         k.smem_v2pc = [](int n, int, bool box) {
             return engine_smem_bytes<R, Cost::A>(n, 32, box, true) + 16 + sizeof(PcEntry<R, Cost::A>) * 3 * 32 * 32;
         };
+        k.v2z = nullptr;
+        k.v2gz = nullptr;
+        k.lazy_radius = nullptr;
+        k.lazy_alpha_of = nullptr;
+        if constexpr (LazyCost<Cost>::value) {
+            k.v2z = reinterpret_cast<const void*>(&v2_lazy_kernel<R, Cost, NT, false>);
+            k.v2gz = reinterpret_cast<const void*>(&v2_lazy_kernel<R, Cost, 0, true>);
+            k.lazy_radius = &LazyCost<Cost>::radius;
+            k.lazy_alpha_of = &LazyCost<Cost>::alpha;
+        }
         if constexpr (PairOf<Cost>::value) {
             k.v1p = reinterpret_cast<const void*>(&v1_pair_kernel<R, Cost, NT>);
             k.v2p = reinterpret_cast<const void*>(&v2_pair_kernel<R, Cost, NT>);

@@ -294,6 +294,62 @@ struct Sphere {
 };
 
 // ------------------------------------------------------------------------
+// Deferred-fold traits (engine.cuh, sweep_lazy)
+//
+// Families whose energy is an affine image of ONE additive fold:
+//   E = finish(s),  s = init (+/-) t_0 (+/-) t_1 ... (+/-) t_{n-1}  (sigma = +1 / -1)
+//   finish(s) = alpha(n) * s, rounded fin_round times.
+// For those the engine tracks S = init + sigma * sum t_k in double and settles
+// a Metropolis decision from an interval around alpha*S whenever the interval
+// is conclusive (engine.cuh explains the bound); term_bound(lo, hi) bounds
+// |t| of a coordinate over [lo, hi] for the computed (rounded) term.
+// ------------------------------------------------------------------------
+
+template <class Fam>
+struct LazyOf {
+    static constexpr bool value = false;
+};
+template <class R>
+struct LazyOf<Schwefel<R>> { // -s/n: one rounding (the division; negation is exact)
+    static constexpr bool value = true;
+    static constexpr int sigma = 1;
+    static constexpr int fin_round = 1;
+    PSA_HD static double alpha(int n) { return -1.0 / static_cast<double>(n); }
+    // |x sin(sqrt|x|)| <= |x| (|sin| <= 1 for the glibc-exact sin)
+    static double term_bound(double lo, double hi) { return fmax(fabs(lo), fabs(hi)); }
+};
+template <class R>
+struct LazyOf<Rastrigin<R>> { // s from init 10n, finish = identity
+    static constexpr bool value = true;
+    static constexpr int sigma = 1;
+    static constexpr int fin_round = 0;
+    PSA_HD static double alpha(int) { return 1.0; }
+    static double term_bound(double lo, double hi) {
+        const double m = fmax(fabs(lo), fabs(hi));
+        return m * m + 10.0;
+    }
+};
+template <class R>
+struct LazyOf<Sphere<R>> {
+    static constexpr bool value = true;
+    static constexpr int sigma = 1;
+    static constexpr int fin_round = 0;
+    PSA_HD static double alpha(int) { return 1.0; }
+    static double term_bound(double lo, double hi) {
+        const double m = fmax(fabs(lo), fabs(hi));
+        return m * m;
+    }
+};
+template <class R>
+struct LazyOf<Michalewicz<R>> { // f = 0 - t_0 - t_1 ...
+    static constexpr bool value = true;
+    static constexpr int sigma = -1;
+    static constexpr int fin_round = 0;
+    PSA_HD static double alpha(int) { return 1.0; }
+    static double term_bound(double, double) { return 1.0; } // |sin(x) s^20| <= 1
+};
+
+// ------------------------------------------------------------------------
 // Full-evaluation families: X(k) returns x_k as Real
 // ------------------------------------------------------------------------
 

@@ -16,13 +16,14 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--n", type=int, default=100)
     ap.add_argument("--chains", type=int, default=1 << 20)
+    ap.add_argument("--t0", type=float, default=1000.0)
     ap.add_argument("--tmin", type=float, default=989.0)  # 1000, 990 -> 2 levels
     ap.add_argument("--precision", default="f32")
     ap.add_argument("--engine", type=int, default=2)
     ap.add_argument("--launches", type=int, default=2)
     a = ap.parse_args()
     f = psa.registry_get("F0_a").with_dim(a.n)
-    cfg = psa.EngineConfig(n_chains=a.chains, schedule=psa.AnnealSchedule(1000.0, a.tmin, 0.99, 100),
+    cfg = psa.EngineConfig(n_chains=a.chains, schedule=psa.AnnealSchedule(a.t0, a.tmin, 0.99, 100),
                            precision=psa.Precision.f32 if a.precision == "f32" else psa.Precision.f64)
     with psa.Plan(f, cfg, engine=a.engine) as p:
         for _ in range(a.launches):

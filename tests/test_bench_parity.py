@@ -62,7 +62,7 @@ def device(gpu_lib, engine, family, dim, chains, sched, prec):
     return as_golden(res.as_dict())
 
 
-@pytest.mark.parametrize("mode", ["", "single"])
+@pytest.mark.parametrize("mode", ["", "single", "pair"])
 @pytest.mark.parametrize("key", ["f32", "f64"])
 def test_c2_full_chain_count_bitwise_vs_reference(gpu_lib, bench_golden, monkeypatch, key, mode):
     rec = bench_golden[f"c2_{key}"]
@@ -74,15 +74,16 @@ def test_c2_full_chain_count_bitwise_vs_reference(gpu_lib, bench_golden, monkeyp
     assert_same(got, rec, f"c2 {key} {mode or 'default'}")
 
 
-def test_c2_bench_kernel_is_the_pair_kernel(gpu_lib):
-    """The default plan at C2 (f32) is the chain-pair kernel — the one the
-    test above pins at full size."""
+def test_c2_bench_kernel_is_the_lazy_kernel(gpu_lib):
+    """The default plan at C2 (f32) is the deferred-fold kernel — the one the
+    test above pins at full size (mode "single" pins the fold-every-trial
+    kernel)."""
     import paper_2408_00018_b200 as psa
     f = psa.registry_get("F0_a").with_dim(100)
     cfg = psa.EngineConfig(n_chains=1 << 20, schedule=psa.AnnealSchedule(1000.0, 989.01, 0.99, 100),
                            precision=psa.Precision.f32)
     with psa.Plan(f, cfg) as p:
-        assert p.description.startswith("v2_pair_kernel"), p.description
+        assert p.description.startswith("v2_lazy_kernel"), p.description
 
 
 @pytest.mark.parametrize("engine", [1, 2])

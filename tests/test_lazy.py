@@ -1,0 +1,110 @@
+"""Deferred-fold engine (v2_lazy_kernel, engine.cuh sweep_lazy) against the
+reference (GPU tests).
+
+The deferred fold settles a Metropolis decision from an energy interval and
+folds the chain's terms only when the interval straddles the threshold, so
+its risk is the bound: a radius that is too small gives a wrong decision.
+These cases aim at the places where the interval is tight or undecided:
+
+  * very low temperatures (every uphill decision sits near the band),
+  * tiny boxes (energy differences of the order of the radius itself, so
+    most decisions take the exact path),
+  * non-uniform boxes, random starts, f32 and f64, compile-time and runtime n,
+    shared-memory and HBM rows,
+and compare bit for bit with the C oracle (oracle/sa_oracle.c, pinned to the
+reference) and with the fold-every-trial kernels (PSA_LAZY=0).
+"""
+import numpy as np
+import pytest
+
+import paper_2408_00018_b200 as psa
+from oracle_lib import Config, Problem, oracle_sync, same_run
+from test_gpu_parity import device_run
+
+pytestmark = pytest.mark.gpu
+
+LAZY = [("SCHWEFEL", -512.0, 512.0), ("RASTRIGIN", -5.12, 5.12), ("SPHERE", -2.0, 2.0),
+        ("MICHALEWICZ", 0.0, 3.141592653589793)]
+
+
+def _plan_desc(family, dim, lo, hi, chains, sched, prec):
+    f = psa.ObjectiveFunction("lazy", "lazy", dim, psa.BoxDomain([lo] * dim, [hi] * dim), family)
+    cfg = psa.EngineConfig(n_chains=chains, schedule=psa.AnnealSchedule(*sched), precision=prec)
+    with psa.Plan(f, cfg) as p:
+        return p.description
+
+
+@pytest.mark.parametrize("family,lo,hi", LAZY)
+@pytest.mark.parametrize("prec", [0, 1])
+@pytest.mark.parametrize("dim", [10, 100, 7])
+def test_lazy_matches_oracle(gpu_lib, family, lo, hi, prec, dim):
+    prob = Problem(family, dim, lo, hi)
+    for start, sched in ((0, (50.0, 0.05, 0.7, 40)), (1, (1e-3, 1e-7, 0.25, 64))):
+        cfg = Config(517, sched, 5 + start, prec, start)
+        got = device_run(2, prob, cfg)
+        want = oracle_sync(prob, cfg)
+        assert not same_run(got, want), (family, dim, prec, start, same_run(got, want))
+
+
+def test_lazy_kernel_is_the_default_for_affine_families(gpu_lib):
+    d = _plan_desc("SCHWEFEL", 100, -512.0, 512.0, 1 << 16, (1000.0, 989.01, 0.99, 100),
+                   psa.Precision.f32)
+    assert d.startswith("v2_lazy_kernel"), d
+
+
+@pytest.mark.parametrize("prec", [0, 1])
+def test_tiny_box_forces_exact_settles(gpu_lib, prec):
+    """Energy differences of the order of the radius: most decisions need the
+    exact folds, and the result must still be the reference's."""
+    # f32 radius ~ 2^-24 of the energy; f64 ~ the double tracking error
+    lo, hi = 1.0, 1.0 + (2.0 ** -18 if prec == 1 else 2.0 ** -44)
+    prob = Problem("SPHERE", 30, lo, hi)
+    cfg = Config(300, (1e-6, 1e-9, 0.3, 50), 3, prec, 1)
+    got = device_run(2, prob, cfg)
+    want = oracle_sync(prob, cfg)
+    assert not same_run(got, want), same_run(got, want)
+    f = psa.ObjectiveFunction("t", "t", 30, psa.BoxDomain([lo] * 30, [hi] * 30), "SPHERE")
+    ecfg = psa.EngineConfig(n_chains=300, schedule=psa.AnnealSchedule(1e-6, 1e-9, 0.3, 50), seed=3,
+                            precision=psa.Precision(prec), start_mode=psa.StartMode.random_per_chain)
+    with psa.Plan(f, ecfg) as p:
+        p.launch()
+        p.fetch()
+        settles = p.exact_settles()
+    assert settles > 0
+
+
+def test_nonuniform_box_matches_oracle(gpu_lib):
+    rng = np.random.default_rng(7)
+    dim = 40
+    lo = -rng.uniform(1, 600, dim)
+    hi = rng.uniform(1, 600, dim)
+    prob = Problem("SCHWEFEL", dim, lo, hi)
+    for prec in (0, 1):
+        cfg = Config(1000, (300.0, 0.01, 0.8, 60), 9, prec, 1)
+        got = device_run(2, prob, cfg)
+        want = oracle_sync(prob, cfg)
+        assert not same_run(got, want), (prec, same_run(got, want))
+
+
+@pytest.mark.parametrize("prec", [0, 1])
+def test_lazy_equals_fold_every_trial_at_scale(gpu_lib, monkeypatch, prec):
+    """65536 chains, n = 100, 40 levels of the paper ladder's tail (the low
+    temperatures where the interval is tightest): bitwise equal to the
+    fold-every-trial kernel."""
+    prob = Problem("SCHWEFEL", 100, -512.0, 512.0)
+    cfg = Config(1 << 16, (0.5, 0.01, 0.9, 100), 21, prec, 1)
+    monkeypatch.delenv("PSA_LAZY", raising=False)
+    lazy = device_run(2, prob, cfg)
+    monkeypatch.setenv("PSA_LAZY", "0")
+    full = device_run(2, prob, cfg)
+    assert not same_run(lazy, full), same_run(lazy, full)
+
+
+@pytest.mark.parametrize("prec", [0, 1])
+def test_lazy_hbm_rows_match_oracle(gpu_lib, monkeypatch, prec):
+    monkeypatch.setenv("PSA_FORCE_HBM_ROWS", "1")
+    prob = Problem("RASTRIGIN", 45, -5.12, 5.12)
+    cfg = Config(700, (20.0, 0.01, 0.75, 70), 4, prec, 1)
+    got = device_run(2, prob, cfg)
+    want = oracle_sync(prob, cfg)
+    assert not same_run(got, want), same_run(got, want)
