@@ -271,6 +271,10 @@ psa_status psa_device_evaluate(const psa_objective* f, int32_t precision, const 
  * 3/4/5 the branch-free hot-loop sqrtf/sinf/cosf with their validity flag in
  * ok[i], 6 the compiler's sqrt.rn.f32) and of sin/cos/exp (fn 0/1/2) */
 psa_status psa_device_libm_f32(int32_t fn, const float* x, int32_t count, float* out, int32_t* ok);
+/* the Metropolis pre-test (engine.cuh metropolis_fast) on `count` draws
+ * placed at the decision boundary: out = {certain, certain but different
+ * from the exact test, undecided} */
+psa_status psa_device_metropolis_check(int32_t precision, uint64_t seed, uint64_t count, uint64_t* out);
 psa_status psa_device_libm_f64(int32_t fn, const double* x, int32_t count, double* out);
 
 /* ---- host restatements of glibc libm used by the device code ------------

@@ -171,6 +171,7 @@ def _declare(lib):
         "psa_plan_set_peers": (st, [C.c_void_p, P(C.c_void_p), C.c_int32]),
         "psa_plan_describe": (st, [C.c_void_p, C.c_char_p, C.c_int32]),
         "psa_plan_stats": (st, [C.c_void_p, P(C.c_uint64)]),
+        "psa_device_metropolis_check": (st, [C.c_int32, C.c_uint64, C.c_uint64, P(C.c_uint64)]),
         "psa_nelder_mead_batch": (st, [P(psa_objective), P(C.c_double), C.c_int32, P(psa_nm_config), P(C.c_double),
                                        P(C.c_double), P(C.c_int32), P(C.c_uint64)]),
         "psa_metropolis_sweep": (st, [P(psa_objective), C.c_int32, P(C.c_double), P(C.c_double), C.c_uint64,
@@ -196,7 +197,7 @@ EXPORTED_SYMBOLS = [
     "psa_libm_exp", "psa_plan_level_detail", "psa_device_libm_f32", "psa_device_libm_f64",
     "psa_plan_create_ex", "psa_plan_mailbox", "psa_plan_mailbox_ipc_handle", "psa_ipc_open",
     "psa_ipc_close", "psa_plan_set_peers", "psa_plan_describe", "psa_metropolis_sweep", "psa_nelder_mead_batch",
-    "psa_plan_stats",
+    "psa_plan_stats", "psa_device_metropolis_check",
 ]
 
 

@@ -265,6 +265,7 @@ struct psa_plan {
     DevBuf<uint32_t> d_masks;
     DevBuf<Cand> d_cand, d_cand_start, d_trace_cand;
     DevBuf<OutScalars> d_out;
+    DevBuf<unsigned long long> d_work; // per-level chain counters (v2_lazy_kernel)
     uint64_t expected_evals = 0, expected_draws = 0;
     // multi-GPU exchange
     int world = 1, rank = 0, max_blocks = 0;
@@ -332,8 +333,12 @@ void plan_build(psa_plan* p, const psa_objective* f, const psa_engine_config* cf
     // Affine families (LazyOf): the deferred-fold sweep settles decisions
     // from an energy interval and folds only when the interval straddles the
     // Metropolis threshold (engine.cuh) — no n-term fold per trial.
+    // With few chains (fewer than 8 warps per SM of one chain per thread) the
+    // producer/consumer kernel's overlap wins (measured: C1, C3), so the
+    // deferred fold is the default only at larger chain counts.
+    const bool few_chains = static_cast<long long>(p->chains_local) < 256ll * lim.sms;
     p->lazy = engine == 2 && p->ks.v2z && !(lazy_env && lazy_env[0] == '0') &&
-              (mode.empty() || mode == "lazy");
+              ((mode.empty() && !few_chains) || mode == "lazy");
     // block size: of 128/96/64/32 threads, the one that keeps the most
     // chain rows resident per SM (large rows: three 32-thread blocks hold
     // more rows than one 64-thread block); ties go to the larger block
@@ -491,6 +496,8 @@ void plan_build(psa_plan* p, const psa_objective* f, const psa_engine_config* cf
     a.level_winner = p->d_winner.p;
     a.level_winner_f = p->d_winner_f.p;
     a.out_scalars = p->d_out.p;
+    p->d_work.alloc(2);
+    a.work = p->d_work.p;
     p->d_error.alloc(1);
     cuda_check(cudaMemset(p->d_error.p, 0, sizeof(int)), "memset");
     a.error_flag = p->d_error.p;
@@ -500,8 +507,9 @@ void plan_build(psa_plan* p, const psa_objective* f, const psa_engine_config* cf
     if (p->lazy) {
         std::vector<double> upper(n);
         for (int k = 0; k < n; ++k) upper[k] = f->lower[k] + width[k];
-        // S is re-summed from V* at every level start: at most N updates
-        a.lazy_r = p->ks.lazy_radius(n, p->N, f->lower, upper.data());
+        a.lazy_r = p->ks.lazy_radius(n, f->lower, upper.data());
+        const char* adapt = std::getenv("PSA_LAZY_ADAPT"); // 0: never fall back (tests)
+        a.lazy_adapt = !(adapt && adapt[0] == '0');
         a.lazy_alpha = p->ks.lazy_alpha_of(n);
     }
     if (p->world > 1) {
@@ -530,6 +538,7 @@ void plan_launch(psa_plan* p, cudaStream_t s) {
     if (p->world > 1 && !p->peers_set)
         fail(PSA_ERR_INVALID_ARGUMENT, "parsa_b200: multi-GPU plan launched before psa_plan_set_peers");
     cuda_check(cudaMemsetAsync(p->d_out.p, 0, sizeof(OutScalars), s), "memset");
+    cuda_check(cudaMemsetAsync(p->d_work.p, 0, 2 * sizeof(unsigned long long), s), "memset");
     p->args.epoch = ++p->epoch; // mailbox records of this launch carry the epoch
     void* params[] = {&p->args};
     if (p->engine == 2) {
@@ -1134,6 +1143,24 @@ psa_status psa_device_libm_f32(int32_t fn, const float* x, int32_t count, float*
                                     params, 0, 0), "probe_libm_f32");
         cuda_check(cudaMemcpy(out, dout.p, sizeof(float) * count, cudaMemcpyDeviceToHost), "D2H");
         if (ok) cuda_check(cudaMemcpy(ok, dok.p, sizeof(int32_t) * count, cudaMemcpyDeviceToHost), "D2H");
+    });
+}
+
+psa_status psa_device_metropolis_check(int32_t precision, uint64_t seed, uint64_t count, uint64_t* out) {
+    return guarded([&] {
+        if (!out) fail(PSA_ERR_INVALID_ARGUMENT, "parsa_b200: null argument");
+        require_device();
+        DevBuf<unsigned long long> d;
+        d.alloc(3);
+        cuda_check(cudaMemset(d.p, 0, 3 * sizeof(unsigned long long)), "memset");
+        unsigned long long c = count;
+        void* params[] = {&seed, &c, &d.p};
+        cuda_check(cudaLaunchKernel(psa::probe_metropolis_kernel(precision == PSA_F32 ? PSA_F32 : PSA_F64),
+                                    dim3(148 * 8), dim3(256), params, 0, 0),
+                   "probe_metropolis");
+        unsigned long long h[3];
+        cuda_check(cudaMemcpy(h, d.p, sizeof(h), cudaMemcpyDeviceToHost), "D2H");
+        for (int i = 0; i < 3; ++i) out[i] = h[i];
     });
 }
 

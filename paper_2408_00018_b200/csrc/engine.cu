@@ -111,6 +111,43 @@ __global__ void probe_libm_f64(int fn, const double* x, int count, double* out) 
     }
 }
 
+// Metropolis pre-test check: draws placed at (and around) the decision
+// boundary dE* = -T ln(u); out = {certain, certain but different from the
+// exact test of sa_core.cpp:46-55, undecided}
+template <class R>
+__global__ void probe_metropolis(uint64_t seed, unsigned long long count, unsigned long long* out) {
+    const PhiloxKeys keys = make_keys(seed);
+    unsigned long long certain = 0, wrong = 0, undecided = 0;
+    const unsigned long long stride = static_cast<unsigned long long>(gridDim.x) * blockDim.x;
+    for (unsigned long long i = static_cast<unsigned long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
+         i += stride) {
+        const uint32_t c = static_cast<uint32_t>(i >> 20), lv = static_cast<uint32_t>(i & 0xfffff);
+        const uint64_t m = draw_bits53(0, c, lv, keys);
+        const double ua = bits_to_uniform(draw_bits53(1, c, lv, keys));
+        const double ub = bits_to_uniform(draw_bits53(2, c, lv, keys));
+        const double uc = bits_to_uniform(draw_bits53(3, c, lv, keys));
+        const double T = exp2(-10.0 + 20.0 * ua);             // 2^-10 .. 2^10
+        const double dstar = -T * log(bits_to_uniform(m));     // the boundary (inf for m = 0)
+        double dd;
+        if ((i & 7) == 0) dd = 2.0 * dstar * ub;               // anywhere below 2 dE*
+        else dd = dstar * (1.0 + (ub < 0.5 ? -1.0 : 1.0) * exp2(-40.0 + 34.0 * uc)); // within 2^-40..2^-6
+        const R E = static_cast<R>(-500.0 + 1000.0 * ub);
+        const R trial = static_cast<R>(static_cast<double>(E) + dd);
+        const int r = metropolis_fast<R>(trial, E, metropolis_k2(T), metropolis_band(m));
+        const double delta = static_cast<double>(trial) - static_cast<double>(E);
+        const bool ref = delta <= 0 || Accept<R>::exact(delta, T, m);
+        if (r < 0) {
+            ++undecided;
+        } else {
+            ++certain;
+            if ((r != 0) != ref) ++wrong;
+        }
+    }
+    atomicAdd(out, certain);
+    atomicAdd(out + 1, wrong);
+    atomicAdd(out + 2, undecided);
+}
+
 template <class R>
 EngineKernels kernels_for(int family, int n) {
 #ifdef PSA_EXPERIMENT_ONLY
@@ -145,5 +182,9 @@ const void* probe_philox_kernel() { return reinterpret_cast<const void*>(&probe_
 const void* v1_finalize_kernel() { return reinterpret_cast<const void*>(&v1_finalize); }
 const void* probe_libm_f32_kernel() { return reinterpret_cast<const void*>(&probe_libm_f32); }
 const void* probe_libm_f64_kernel() { return reinterpret_cast<const void*>(&probe_libm_f64); }
+const void* probe_metropolis_kernel(int precision) {
+    return precision == PSA_F32 ? reinterpret_cast<const void*>(&probe_metropolis<float>)
+                                : reinterpret_cast<const void*>(&probe_metropolis<double>);
+}
 
 } // namespace psa

@@ -283,13 +283,17 @@ PSA_DEV float lg2_approx(float x) {
 //    x = dE*log2(e)/T <= L = -log2(u).  The device forms x = float(d)*k2
 //    (k2 = log2(e)/T rounded to a normal float: relative error below 2^-22
 //    in all) and, from the acceptance draw alone, the band [lo, hi] =
-//    [L - 2^-10, L + 2^-10] with L = 53 - lg2.approx(float(m)) (MUFU.LG2's
+//    [L - 2^-13, L + 2^-13] with L = 53 - lg2.approx(float(m)) (MUFU.LG2's
 //    error, 2^-22 absolute, or even relative to |log2| <= 53, plus float(m)'s
 //    rounding stay below 2^-16 for u = m*2^-53, m >= 1; L <= 53).  x < lo accepts and
 //    x > hi rejects with certainty: the errors of x (|x| * 2^-22 < 2^-15 for
 //    |x| <= 60; a larger x is far beyond hi), of L, and of the reference's own
 //    exp / expf rounding and float(u) (relative 2^-23 each, below 2^-22 in
-//    the log domain) are all far inside the 2^-10 margin.  m == 0, NaNs, a
+//    the log domain) add up to about 2^-15, inside the 2^-13 margin (the
+//    margin was 2^-10 in round 1; every undecided draw costs the exact test,
+//    and in the deferred-fold sweep two folds, so it is as small as the error
+//    budget allows — psa_device_metropolis_check counts disagreements with
+//    the exact test on draws placed at the boundary).  m == 0, NaNs, a
 //    k2 outside the normal floats and the band itself report undecided and
 //    the caller runs the exact glibc-restated test.
 //  * The band depends only on the draw, which the counter-based streams give
@@ -302,7 +306,7 @@ struct MBand {
 PSA_DEV MBand metropolis_band(uint64_t m) {
     const float l = lg2_approx(__ull2float_rn(m));
     const float nan = __int_as_float(0x7fffffff);
-    return MBand{m ? 0x1.a7fep+5f - l : nan, m ? 0x1.a802p+5f - l : nan}; // 53 -/+ 2^-10
+    return MBand{m ? 0x1.a7ffcp+5f - l : nan, m ? 0x1.a8004p+5f - l : nan}; // 53 -/+ 2^-13
 }
 
 // log2(e) / T as the pre-test's factor; NaN (always undecided) unless normal
@@ -456,50 +460,38 @@ PSA_DEV R sweep(Row row, int n_rt, int family, R E, double temperature, uint32_t
 // Deferred fold: Metropolis decisions from an energy interval
 //
 // For the affine families of objectives.cuh (LazyOf: E = finish(s), s one
-// additive fold of the cached terms) a trial's exact energy is only needed
-// when its decision depends on the last bits.  The sweep tracks, per chain,
-//   S  = init + sigma * sum_k t_k   in double (one add per accepted move),
-// and knows a radius rE (host-computed, lazy_radius below) such that the
-// exact binary32/binary64 energy the reference computes — the fold in index
-// order, then finish — lies in [alpha*S - rE, alpha*S + rE]:
-//   * fold rounding: each of the n adds rounds by at most u|partial|, and
-//     |partial_k| <= |init| + sum_{j<=k} |t_j|, so the fold is within
-//     u(1+nu) (n|init| + sum_k (n-k) Tmax_k) of the exact sum (Tmax_k bounds
-//     |t_k| over the box, LazyOf::term_bound);
-//   * the double tracking of S adds at most 2^-53 (|init| + sum Tmax) per
-//     add (n adds at the level start, two per update);
-//   * finish rounds fin_round times (u relative), the double arithmetic of
-//     the centre and the interval ends adds 2^-48 of the largest energy.
-// The old energy is either exact (after a fold: radius 0) or such an
-// interval.  With d in [lo, hi] the decision of sa_core.cpp:46-55 is certain
-// when hi <= 0 or x(hi) < band.lo (accept: every d in the interval accepts,
-// x is monotone in d) or when lo > 0 and x(lo) > band.hi (reject) — the same
-// log-domain band as metropolis_fast, whose margin already covers the
+// additive fold of the cached terms, finish(s) = alpha*s up to fin_round
+// roundings) a trial's exact energy matters only when its decision depends
+// on the last bits.  Let S(X) = init + sigma * sum_k t_k be the exact real
+// sum of a state's terms.  The energy the reference computes — the fold in
+// index order in R, then finish — satisfies |E(X) - alpha S(X)| <= rE for
+// every state of the box (lazy_radius, host):
+//   * each of the n fold adds rounds by at most u|partial|, and |partial_k|
+//     <= |init| + sum_{j<=k} Tmax_j (Tmax_k bounds |t_k| over the box,
+//     LazyOf::term_bound), so the fold is within u(1+2nu)(n|init| +
+//     sum_k (n-k) Tmax_k) of S;
+//   * finish rounds fin_round times (u relative to the largest |E|).
+// A trial changes one term, so S(trial) - S(old) = sigma (t' - t_d) exactly,
+// and the reference's difference d = E(trial) - E(old) lies within
+//   q +- rr,   q = alpha * sigma * (t' - t_d)  (computed in R),
+// rr = 2 rE plus the rounding of q and of the interval ends (host margin).
+// No running sum is kept: the interval comes from the two cached terms.
+// The decision of sa_core.cpp:46-55 is certain when hi = q + rr <= 0 or
+// x(hi) < band.lo (accept: every d of the interval accepts, and x is
+// monotone in d) or when lo = q - rr > 0 and x(lo) > band.hi (reject) — the
+// log-domain band of metropolis_fast, whose 2^-13 margin already covers the
 // rounding of x.  Otherwise (a warp-uniform rare branch) the old state and
 // the trial are folded exactly and metropolis_fast / Accept::exact decide as
-// in sweep().  Decisions are therefore identical to the reference's, and the
-// energies that leave the sweep (its end energy, every energy compared in a
-// settled decision) are the exact folds.  An accepted move writes its term to
-// the row; a rejected one touches nothing.  NaN/inf anywhere makes every
+// in sweep().  Decisions are therefore the reference's; the energies that
+// leave the sweep (the end energy, every energy compared in a settled
+// decision) are exact folds.  An accepted move writes its term to the row,
+// a rejected one touches nothing.  NaN or inf anywhere makes every
 // comparison false, i.e. the exact path.
 // ---------------------------------------------------------------------------
 
-// S of a row: init, then sigma * t_k in index order (double)
-template <class Fam, class Row>
-PSA_DEV double lazy_sum(const Row& row, int n) {
-    using L = LazyOf<Fam>;
-    double s = static_cast<double>(Fam::init(0, n));
-    for (int k = 0; k < n; ++k) {
-        const double t = static_cast<double>(row[k]);
-        s = L::sigma > 0 ? s + t : s - t;
-    }
-    return s;
-}
-
-// the radius rE of the interval (host); updates = moves applied to S since
-// it was last summed from a row
+// the half-width rr of the interval of d (host)
 template <class R, template <class> class F>
-double lazy_radius(int n, long long updates, const double* lower, const double* upper) {
+double lazy_radius(int n, const double* lower, const double* upper) {
     using Fam = F<R>;
     using L = LazyOf<Fam>;
     const double u = sizeof(R) == 4 ? 0x1.0p-24 : 0x1.0p-53;
@@ -511,28 +503,31 @@ double lazy_radius(int n, long long updates, const double* lower, const double* 
         wmax += static_cast<double>(n - k) * t;
         tmax = fmax(tmax, t);
     }
-    const double P = init + tsum;                  // bounds |S| and every partial sum
     const double a = fabs(L::alpha(n));
     const double fold = u * (1.0 + 2.0 * n * u) * (static_cast<double>(n) * init + wmax);
-    const double eta = 0x1.0p-53 * (static_cast<double>(n) * P + static_cast<double>(updates + 1) * (2.0 * tmax + P));
-    const double cmax = a * P;
-    const double r = a * (fold + eta) + L::fin_round * u * cmax + 0x1.0p-48 * cmax;
-    return r * 1.01;
+    const double cmax = a * (init + tsum);                   // bounds |E|
+    const double rE = a * fold + L::fin_round * u * cmax;    // |E - alpha S|
+    const double margin = 32.0 * u * a * tmax + 4.0 * u * cmax; // q, alpha, hi/lo roundings
+    return (2.0 * rE + margin) * 1.01;
 }
 
+#ifndef PSA_LAZY_UNROLL
+#define PSA_LAZY_UNROLL 1
+#endif
+constexpr int kLazyUnroll = PSA_LAZY_UNROLL;
+
 template <class R, class Cost, int NT = 0, class Row = R*>
-PSA_DEV R sweep_lazy(Row row, int n_rt, int family, R E, double S, double temperature, uint32_t chain,
-                     uint32_t level, uint32_t ctr, int N, const Box& box, const PhiloxKeys& keys,
-                     uint32_t* mask, size_t mask_stride, double* x, size_t x_stride, SweepStats& st,
-                     double rE, double alpha) {
+PSA_DEV R sweep_lazy(Row row, int n_rt, int family, R E, double temperature, uint32_t chain, uint32_t level,
+                     uint32_t ctr, int N, const Box& box, const PhiloxKeys& keys, uint32_t* mask,
+                     size_t mask_stride, double* x, size_t x_stride, SweepStats& st, R rr, R alpha) {
     using L = LazyOf<typename Cost::Fam>;
     static_assert(Cost::A == 1, "deferred fold: one accumulator");
     const int n = NT > 0 ? NT : n_rt;
     const float k2 = metropolis_k2(temperature);
     const PhiloxChain pc = philox_chain(chain, level, keys);
     const double idx_scale = static_cast<double>(n) * 0x1.0p-53;
-    double co = static_cast<double>(E); // old energy in [co - ro, co + ro]; ro == 0: exact
-    double ro = 0.0;
+    const R sa = L::sigma > 0 ? alpha : -alpha;
+    bool have = true; // E is the exact energy of the row
     int d;
     double xnew;
     R tn[1];
@@ -552,6 +547,7 @@ PSA_DEV R sweep_lazy(Row row, int n_rt, int family, R E, double S, double temper
     for (int j0 = 0; j0 < N; j0 += 32) {
         const int jn = N - j0 < 32 ? N - j0 : 32;
         uint32_t word = 0;
+#pragma unroll kLazyUnroll
         for (int j = 0; j < jn; ++j) {
             const R to = row[d];
             const int dn = min(static_cast<int>(static_cast<double>(q1) * idx_scale), n - 1);
@@ -564,48 +560,38 @@ PSA_DEV R sweep_lazy(Row row, int n_rt, int family, R E, double S, double temper
             const uint64_t r3 = draw_bits53_fast(ctr + 8, pc, keys);
             const MBand b3 = metropolis_band(m3);
             // the interval decision
-            const double dl = static_cast<double>(tn[0]) - static_cast<double>(to);
-            const double St = L::sigma > 0 ? S + dl : S - dl;
-            const double ct = alpha * St;
-            const double dh = ct - co, rr = rE + ro;
-            const double hi = dh + rr, lo = dh - rr;
+            const R q = (tn[0] - to) * sa;
+            const R hi = q + rr, lo = q - rr;
             const float xh = static_cast<float>(hi) * k2, xl = static_cast<float>(lo) * k2;
-            int r = ((hi <= 0.0) | (xh < b3.lo)) ? 1 : (((lo > 0.0) & (xl > b3.hi)) ? 0 : -1);
+            int r = ((hi <= R(0)) | (xh < b3.lo)) ? 1 : (((lo > R(0)) & (xl > b3.hi)) ? 0 : -1);
             if (__any_sync(__activemask(), !ok))
                 if (!ok) Cost::cache(static_cast<R>(xn), dn, n, tnn);
             bool settled = false;
             if (__any_sync(__activemask(), r < 0)) {
-                // rare: fold exactly (the whole warp folds; every lane with an
-                // interval energy takes the exact old value for free)
-                if (__any_sync(__activemask(), (r < 0) & (ro != 0.0))) {
+                // rare: fold exactly (the whole warp folds; every lane whose
+                // energy is stale takes the exact old value for free)
+                if (__any_sync(__activemask(), (r < 0) & !have)) {
                     const R eo = row_energy<Cost, NT>(row, n, family);
-                    if (ro != 0.0) {
-                        co = static_cast<double>(eo);
-                        ro = 0.0;
+                    if (!have) {
+                        E = eo;
+                        have = true;
                     }
                 }
                 if (r < 0) row[d] = tn[0];
                 const R et = row_energy<Cost, NT>(row, n, family);
                 if (r < 0) {
-                    int q = metropolis_fast<R>(et, static_cast<R>(co), k2, b3);
-                    if (q < 0) q = Accept<R>::exact(static_cast<double>(et) - co, temperature, m3);
-                    if (q) {
-                        co = static_cast<double>(et);
-                        ro = 0.0;
-                        S = St;
-                    } else {
-                        row[d] = to;
-                    }
-                    r = q;
+                    int v = metropolis_fast<R>(et, E, k2, b3);
+                    if (v < 0) v = Accept<R>::exact(static_cast<double>(et) - static_cast<double>(E), temperature, m3);
+                    if (v) E = et;
+                    else row[d] = to;
+                    r = v;
                     settled = true;
                     st.settles += 1;
                 }
             }
             if (r && !settled) {
                 row[d] = tn[0];
-                S = St;
-                co = ct;
-                ro = rE;
+                have = false;
             }
             ctr += 3;
             if (r) {
@@ -623,13 +609,13 @@ PSA_DEV R sweep_lazy(Row row, int n_rt, int family, R E, double S, double temper
         if (mask) mask[static_cast<size_t>(j0 >> 5) * mask_stride] = word;
     }
     // the end energy is the exact fold
-    if (__any_sync(__activemask(), ro != 0.0)) {
+    if (__any_sync(__activemask(), !have)) {
         const R e = row_energy<Cost, NT>(row, n, family);
-        if (ro != 0.0) co = static_cast<double>(e);
+        if (!have) E = e;
     }
     st.evals += static_cast<uint64_t>(N);
     st.draws += 3ull * static_cast<uint64_t>(N);
-    return static_cast<R>(co);
+    return E;
 }
 
 // ---------------------------------------------------------------------------

@@ -66,9 +66,12 @@ struct EngineArgs {
     char* const* mail_peers; // device array: every GPU's mailbox as seen from here
     long long spin_limit;   // clock64 cycles before a missing peer is reported
     int* error_flag;
-    // deferred fold (v2_lazy_kernel): energy radius and finish slope
+    // deferred fold (v2_lazy_kernel): half-width of the interval of the
+    // energy difference, and the finish slope
     double lazy_r;
     double lazy_alpha;
+    unsigned long long* work; // [2] per-level chain counters (dynamic assignment)
+    int lazy_adapt;           // switch a block to fold-every-trial when settles pass 2%
 };
 
 struct NMOut {
@@ -143,7 +146,7 @@ struct EngineKernels {
     // deferred fold (LazyOf families), else nullptr
     const void* v2z;  // shared-memory rows
     const void* v2gz; // HBM rows
-    double (*lazy_radius)(int n, long long updates, const double* lower, const double* upper);
+    double (*lazy_radius)(int n, const double* lower, const double* upper);
     double (*lazy_alpha_of)(int n);
 };
 
@@ -155,5 +158,6 @@ const void* probe_libm_f32_kernel();
 const void* nm_kernel_for(int family);
 size_t nm_smem_bytes(int n, int cluster_ctas, bool q_smem);
 const void* probe_libm_f64_kernel();
+const void* probe_metropolis_kernel(int precision);
 
 } // namespace psa

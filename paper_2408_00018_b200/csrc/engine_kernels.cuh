@@ -80,10 +80,11 @@ size_t engine_smem_bytes(int n, int B, bool box, bool rows_in_smem, bool pair = 
 
 struct SharedScalars {
     double estar;
-    double sstar; // deferred fold: S of the level start (lazy_sum of V*)
     double best_f;
     int32_t best_c;
-    int32_t pad;
+    int32_t fold_mode;               // deferred-fold kernel: fold every trial from now on
+    unsigned long long lv_settles;   // deferred-fold kernel: this level's exact settles
+    unsigned long long lv_chains;    //   and chains swept by the block
 };
 
 template <class R, class Cost>
@@ -435,9 +436,11 @@ __device__ __forceinline__ void v2_body(const EngineArgs& a) {
     __syncthreads();
     if (tid == 0) {
         sh->estar = static_cast<double>(Cost::template energy<NT>(vs, n, a.family));
-        if constexpr (LZ) sh->sstar = lazy_sum<typename Cost::Fam>(vs, n);
         sh->best_f = __longlong_as_double(0x7ff0000000000000ll);
         sh->best_c = 0;
+        sh->fold_mode = 0;
+        sh->lv_settles = 0;
+        sh->lv_chains = 0;
     }
     __syncthreads();
 
@@ -548,8 +551,15 @@ __device__ __forceinline__ void v2_body(const EngineArgs& a) {
                 const Cand m2{static_cast<double>(eB), static_cast<int32_t>(cB), 0};
                 if (vB && better(m2, best)) best = m2;
             }
-        } else
-        for (size_t cl = gtid; cl < a.chains_local; cl += total_threads) {
+        } else {
+        // deferred fold: a block whose exact settles passed 2% of its trials
+        // (each costs the warp two folds) sweeps with a fold per trial from
+        // then on — temperatures only fall along the ladder, and the settle
+        // rate with them (large n at low T); both sweeps are exact
+        const bool fold_mode = LZ && sh->fold_mode;
+        const uint64_t settles0 = st.settles;
+        unsigned long long my_chains = 0;
+        auto one_chain = [&](size_t cl) {
             const uint32_t c = static_cast<uint32_t>(a.chain_begin + cl);
             R e;
             uint32_t ctr = 0;
@@ -570,21 +580,57 @@ __device__ __forceinline__ void v2_body(const EngineArgs& a) {
                 e = estar;
             }
             if (l == 0) st.evals += 1; // the start evaluation (engines.cpp:157)
-            if constexpr (LZ) {
-                const double s0 = (l == 0 && a.random_start) ? lazy_sum<typename Cost::Fam>(row, n) : sh->sstar;
-                e = sweep_lazy<R, Cost, NT>(row, n, a.family, e, s0, temperature, c, static_cast<uint32_t>(l), ctr,
-                                            a.N, box, a.keys, masks + cl, a.mask_stride, nullptr, 0, st, a.lazy_r,
-                                            a.lazy_alpha);
+            bool lazy = false;
+            if constexpr (LZ) lazy = !fold_mode;
+            if (lazy) {
+                if constexpr (LZ)
+                    e = sweep_lazy<R, Cost, NT>(row, n, a.family, e, temperature, c, static_cast<uint32_t>(l), ctr,
+                                                a.N, box, a.keys, masks + cl, a.mask_stride, nullptr, 0, st,
+                                                static_cast<R>(a.lazy_r), static_cast<R>(a.lazy_alpha));
+                ++my_chains;
             } else {
                 e = sweep<R, Cost, NT>(row, n, a.family, e, temperature, c, static_cast<uint32_t>(l), ctr,
                                        a.N, box, a.keys, masks + cl, a.mask_stride, nullptr, 0, st);
             }
             const Cand mine{static_cast<double>(e), static_cast<int32_t>(c), 0};
             if (better(mine, best)) best = mine;
+        };
+        if constexpr (LZ) {
+            // Dynamic chain assignment: each warp takes the next 32 chains
+            // of the level from a global counter (a chain's sweep time varies
+            // with its exact-fold settles and the scheduler), so the level
+            // ends one chain sweep after the last grab instead of after the
+            // slowest warp's fixed share.  Level l uses work[l & 1]; block 0
+            // clears the other counter, whose last use (level l - 1) ended
+            // before this level's grid barrier and whose next use (level
+            // l + 1) starts after the next one.
+            if (blockIdx.x == 0 && tid == 0) a.work[(l + 1) & 1] = 0;
+            unsigned long long* wc = a.work + (l & 1);
+            const int lane = tid & 31;
+            for (;;) {
+                unsigned long long base = 0;
+                if (lane == 0) base = atomicAdd(wc, 32ull);
+                base = __shfl_sync(0xffffffffu, base, 0);
+                if (base >= a.chains_local) break;
+                if (base + lane < a.chains_local) one_chain(static_cast<size_t>(base + lane));
+            }
+            if (!fold_mode) {
+                atomicAdd(&sh->lv_settles, static_cast<unsigned long long>(st.settles - settles0));
+                atomicAdd(&sh->lv_chains, my_chains);
+            }
+        } else {
+            for (size_t cl = gtid; cl < a.chains_local; cl += total_threads) one_chain(cl);
+        }
         }
         // block argmin -> cand[l&1][block]
         best = block_argmin(best, scratch);
         if (l == 0 && a.random_start) sbest = block_argmin(sbest, scratch);
+        if (LZ && tid == 0) {
+            if (a.lazy_adapt && sh->lv_settles * 50ull > sh->lv_chains * static_cast<unsigned long long>(a.N))
+                sh->fold_mode = 1;
+            sh->lv_settles = 0;
+            sh->lv_chains = 0;
+        }
         if (tid == 0) {
             a.cand[static_cast<size_t>(l & 1) * gridDim.x + blockIdx.x] = best;
             if (l == 0 && a.random_start) a.cand_start[blockIdx.x] = sbest;
@@ -628,10 +674,7 @@ __device__ __forceinline__ void v2_body(const EngineArgs& a) {
         }
         cache_point<R, Cost>(xs, vs, n, a.family);
         __syncthreads();
-        if (tid == 0) {
-            sh->estar = w.e;
-            if constexpr (LZ) sh->sstar = lazy_sum<typename Cost::Fam>(vs, n);
-        }
+        if (tid == 0) sh->estar = w.e;
         __syncthreads();
         if (blockIdx.x == 0) {
             const bool improve = w.e < sh->best_f; // engines.cpp:193 (strict)
@@ -1209,8 +1252,8 @@ struct LazyCost {
 template <class R, template <class> class F>
 struct LazyCost<SepCost<R, F>> {
     static constexpr bool value = LazyOf<F<R>>::value;
-    static double radius(int n, long long updates, const double* lo, const double* hi) {
-        if constexpr (LazyOf<F<R>>::value) return lazy_radius<R, F>(n, updates, lo, hi);
+    static double radius(int n, const double* lo, const double* hi) {
+        if constexpr (LazyOf<F<R>>::value) return lazy_radius<R, F>(n, lo, hi);
         else return -1.0;
     }
     static double alpha(int n) {

@@ -23,6 +23,13 @@ from test_gpu_parity import device_run
 
 pytestmark = pytest.mark.gpu
 
+@pytest.fixture(autouse=True)
+def _lazy_kernel(monkeypatch):
+    """small chain counts default to the producer/consumer kernel; these
+    tests pin the deferred-fold one"""
+    monkeypatch.setenv("PSA_V2_MODE", "lazy")
+
+
 LAZY = [("SCHWEFEL", -512.0, 512.0), ("RASTRIGIN", -5.12, 5.12), ("SPHERE", -2.0, 2.0),
         ("MICHALEWICZ", 0.0, 3.141592653589793)]
 
@@ -52,10 +59,14 @@ def test_lazy_kernel_is_the_default_for_affine_families(gpu_lib):
     assert d.startswith("v2_lazy_kernel"), d
 
 
+@pytest.mark.parametrize("adapt", ["0", "1"])
 @pytest.mark.parametrize("prec", [0, 1])
-def test_tiny_box_forces_exact_settles(gpu_lib, prec):
+def test_tiny_box_forces_exact_settles(gpu_lib, monkeypatch, prec, adapt):
     """Energy differences of the order of the radius: most decisions need the
-    exact folds, and the result must still be the reference's."""
+    exact folds, and the result must still be the reference's — with every
+    settle taken in the deferred-fold sweep (adapt 0) and with the blocks
+    falling back to a fold per trial after the first level (adapt 1)."""
+    monkeypatch.setenv("PSA_LAZY_ADAPT", adapt)
     # f32 radius ~ 2^-24 of the energy; f64 ~ the double tracking error
     lo, hi = 1.0, 1.0 + (2.0 ** -18 if prec == 1 else 2.0 ** -44)
     prob = Problem("SPHERE", 30, lo, hi)
@@ -94,6 +105,7 @@ def test_lazy_equals_fold_every_trial_at_scale(gpu_lib, monkeypatch, prec):
     prob = Problem("SCHWEFEL", 100, -512.0, 512.0)
     cfg = Config(1 << 16, (0.5, 0.01, 0.9, 100), 21, prec, 1)
     monkeypatch.delenv("PSA_LAZY", raising=False)
+    monkeypatch.delenv("PSA_V2_MODE", raising=False)
     lazy = device_run(2, prob, cfg)
     monkeypatch.setenv("PSA_LAZY", "0")
     full = device_run(2, prob, cfg)
@@ -108,3 +120,18 @@ def test_lazy_hbm_rows_match_oracle(gpu_lib, monkeypatch, prec):
     got = device_run(2, prob, cfg)
     want = oracle_sync(prob, cfg)
     assert not same_run(got, want), same_run(got, want)
+
+
+@pytest.mark.parametrize("prec", [0, 1])
+def test_metropolis_pretest_never_contradicts_the_exact_test(gpu_lib, prec):
+    """2^30 acceptance draws placed within 2^-40..2^-6 (relative) of the
+    decision boundary -T ln(u), T in 2^-10..2^10: every decision the band
+    pre-test calls certain equals the glibc-exact test (sa_core.cpp:46-55)."""
+    import ctypes as C
+    out = (C.c_uint64 * 3)()
+    rc = gpu_lib.psa_device_metropolis_check(prec, 12345 + prec, 1 << 30, out)
+    assert rc == 0, gpu_lib.psa_last_error().decode()
+    certain, wrong, undecided = out
+    assert certain + undecided == 1 << 30
+    assert wrong == 0, (certain, wrong, undecided)
+    assert certain > (1 << 30) // 8  # the draws away from the boundary are settled by the band
