@@ -515,6 +515,11 @@ double lazy_radius(int n, const double* lower, const double* upper) {
 #define PSA_LAZY_UNROLL 1
 #endif
 constexpr int kLazyUnroll = PSA_LAZY_UNROLL;
+constexpr unsigned kFullWarp = 0xffffffffu;
+
+// sweep_lazy is called by all 32 lanes of a warp together (the caller runs
+// idle lanes on a duplicate chain with mask == nullptr and a scratch
+// SweepStats), so its votes take the full mask: no divergence checks.
 
 template <class R, class Cost, int NT = 0, class Row = R*>
 PSA_DEV R sweep_lazy(Row row, int n_rt, int family, R E, double temperature, uint32_t chain, uint32_t level,
@@ -564,13 +569,14 @@ PSA_DEV R sweep_lazy(Row row, int n_rt, int family, R E, double temperature, uin
             const R hi = q + rr, lo = q - rr;
             const float xh = static_cast<float>(hi) * k2, xl = static_cast<float>(lo) * k2;
             int r = ((hi <= R(0)) | (xh < b3.lo)) ? 1 : (((lo > R(0)) & (xl > b3.hi)) ? 0 : -1);
-            if (__any_sync(__activemask(), !ok))
-                if (!ok) Cost::cache(static_cast<R>(xn), dn, n, tnn);
             bool settled = false;
-            if (__any_sync(__activemask(), r < 0)) {
+            // one warp vote on the common path for both rare cases
+            if (__any_sync(kFullWarp, (!ok) | (r < 0))) {
+                if (!ok) Cost::cache(static_cast<R>(xn), dn, n, tnn); // general term path
+            if (__any_sync(kFullWarp, r < 0)) {
                 // rare: fold exactly (the whole warp folds; every lane whose
                 // energy is stale takes the exact old value for free)
-                if (__any_sync(__activemask(), (r < 0) & !have)) {
+                if (__any_sync(kFullWarp, (r < 0) & !have)) {
                     const R eo = row_energy<Cost, NT>(row, n, family);
                     if (!have) {
                         E = eo;
@@ -588,6 +594,7 @@ PSA_DEV R sweep_lazy(Row row, int n_rt, int family, R E, double temperature, uin
                     settled = true;
                     st.settles += 1;
                 }
+            }
             }
             if (r && !settled) {
                 row[d] = tn[0];
@@ -609,7 +616,7 @@ PSA_DEV R sweep_lazy(Row row, int n_rt, int family, R E, double temperature, uin
         if (mask) mask[static_cast<size_t>(j0 >> 5) * mask_stride] = word;
     }
     // the end energy is the exact fold
-    if (__any_sync(__activemask(), !have)) {
+    if (__any_sync(kFullWarp, !have)) {
         const R e = row_energy<Cost, NT>(row, n, family);
         if (!have) E = e;
     }

@@ -559,8 +559,12 @@ __device__ __forceinline__ void v2_body(const EngineArgs& a) {
         const bool fold_mode = LZ && sh->fold_mode;
         const uint64_t settles0 = st.settles;
         unsigned long long my_chains = 0;
-        auto one_chain = [&](size_t cl) {
+        // live == false (deferred fold only): an idle lane of the last
+        // group sweeps a duplicate of a live chain so the warp stays whole;
+        // nothing of it is recorded
+        auto one_chain = [&](size_t cl, bool live) {
             const uint32_t c = static_cast<uint32_t>(a.chain_begin + cl);
+            const SweepStats st0 = st; // restored for an idle lane
             R e;
             uint32_t ctr = 0;
             if (l == 0 && a.random_start) {
@@ -574,7 +578,7 @@ __device__ __forceinline__ void v2_body(const EngineArgs& a) {
                 ctr = static_cast<uint32_t>(n);
                 st.draws += static_cast<uint64_t>(n);
                 const Cand s = start_cand(static_cast<double>(e), static_cast<int32_t>(c));
-                if (better(s, sbest)) sbest = s;
+                if (live && better(s, sbest)) sbest = s;
             } else {
                 for (int k = 0; k < n * A; ++k) row[k] = vs[k];
                 e = estar;
@@ -585,15 +589,18 @@ __device__ __forceinline__ void v2_body(const EngineArgs& a) {
             if (lazy) {
                 if constexpr (LZ)
                     e = sweep_lazy<R, Cost, NT>(row, n, a.family, e, temperature, c, static_cast<uint32_t>(l), ctr,
-                                                a.N, box, a.keys, masks + cl, a.mask_stride, nullptr, 0, st,
-                                                static_cast<R>(a.lazy_r), static_cast<R>(a.lazy_alpha));
-                ++my_chains;
+                                                a.N, box, a.keys, live ? masks + cl : nullptr, a.mask_stride,
+                                                nullptr, 0, st, static_cast<R>(a.lazy_r),
+                                                static_cast<R>(a.lazy_alpha));
+                my_chains += live;
             } else {
                 e = sweep<R, Cost, NT>(row, n, a.family, e, temperature, c, static_cast<uint32_t>(l), ctr,
-                                       a.N, box, a.keys, masks + cl, a.mask_stride, nullptr, 0, st);
+                                       a.N, box, a.keys, live ? masks + cl : nullptr, a.mask_stride, nullptr, 0,
+                                       st);
             }
             const Cand mine{static_cast<double>(e), static_cast<int32_t>(c), 0};
-            if (better(mine, best)) best = mine;
+            if (live && better(mine, best)) best = mine;
+            if (!live) st = st0;
         };
         if constexpr (LZ) {
             // Dynamic chain assignment: each warp takes the next 32 chains
@@ -612,14 +619,15 @@ __device__ __forceinline__ void v2_body(const EngineArgs& a) {
                 if (lane == 0) base = atomicAdd(wc, 32ull);
                 base = __shfl_sync(0xffffffffu, base, 0);
                 if (base >= a.chains_local) break;
-                if (base + lane < a.chains_local) one_chain(static_cast<size_t>(base + lane));
+                const bool live = base + lane < a.chains_local;
+                one_chain(static_cast<size_t>(live ? base + lane : base), live);
             }
             if (!fold_mode) {
                 atomicAdd(&sh->lv_settles, static_cast<unsigned long long>(st.settles - settles0));
                 atomicAdd(&sh->lv_chains, my_chains);
             }
         } else {
-            for (size_t cl = gtid; cl < a.chains_local; cl += total_threads) one_chain(cl);
+            for (size_t cl = gtid; cl < a.chains_local; cl += total_threads) one_chain(cl, true);
         }
         }
         // block argmin -> cand[l&1][block]
