@@ -325,8 +325,8 @@ void plan_build(psa_plan* p, const psa_objective* f, const psa_engine_config* cf
     const size_t smem_cap = lim.smem_optin;
     auto smem_of = [&](int B) { return engine == 1 ? p->ks.smem_v1(n, B, !uniform) : p->ks.smem_v2(n, B, !uniform); };
     // Kernel choice (all variants are bit-identical; PSA_V2_MODE = single |
-    // pair | pc | lazy forces one for A/B measurements, PSA_LAZY=0 turns the
-    // deferred fold off).
+    // pair | pc | lazy | lazy1 | lazypair forces one for A/B measurements and
+    // tests, PSA_LAZY=0 turns the deferred fold off).
     const char* mode_env = std::getenv("PSA_V2_MODE");
     const std::string mode = mode_env ? mode_env : "";
     const char* lazy_env = std::getenv("PSA_LAZY");
@@ -338,12 +338,12 @@ void plan_build(psa_plan* p, const psa_objective* f, const psa_engine_config* cf
     // deferred fold is the default only at larger chain counts.
     const bool few_chains = static_cast<long long>(p->chains_local) < 256ll * lim.sms;
     p->lazy = engine == 2 && p->ks.v2z && !(lazy_env && lazy_env[0] == '0') &&
-              ((mode.empty() && !few_chains) || mode == "lazy");
+              ((mode.empty() && !few_chains) || mode == "lazy" || mode == "lazy1" || mode == "lazypair");
     // block size: of 128/96/64/32 threads, the one that keeps the most
     // chain rows resident per SM (large rows: three 32-thread blocks hold
     // more rows than one 64-thread block); ties go to the larger block
     auto kern_of = [&](bool g) {
-        if (p->lazy) return g ? p->ks.v2gz : p->ks.v2z;
+        if (p->lazy) return g ? p->ks.v2gz : uniform ? p->ks.v2zu : p->ks.v2z;
         return engine == 1 ? (g ? p->ks.v1g : p->ks.v1) : (g ? p->ks.v2g : p->ks.v2);
     };
     int B = 32;
@@ -399,8 +399,12 @@ void plan_build(psa_plan* p, const psa_objective* f, const psa_engine_config* cf
     // the pair kernel still keeps >= 8 warps per SM resident and there are
     // enough pairs to fill them (small chain counts or large n keep one chain
     // per thread; PSA_V2_MODE=pair forces pairs whenever the rows fit).
-    const void* pair_kern = engine == 2 ? p->ks.v2p : p->ks.v1p;
-    if (!p->lazy && !p->pc && !p->hbm_rows && pair_kern && mode != "single" && mode != "pc") {
+    // (the deferred fold has a pair form too: v2_lazy_pair_kernel; "lazy1"
+    // forces its one-chain form)
+    // (measured: the pair form is no faster than one chain per thread, so
+    // it runs only when forced)
+    const void* pair_kern = p->lazy ? (mode == "lazypair" ? p->ks.v2pz : nullptr) : engine == 2 ? p->ks.v2p : p->ks.v1p;
+    if (!p->pc && !p->hbm_rows && pair_kern && mode != "single" && mode != "pc" && mode != "lazy1") {
         int Bp = 128;
         while (Bp > 32 && p->ks.smem_v2p(n, Bp, !uniform) > smem_cap) Bp /= 2;
         const size_t smem_p = p->ks.smem_v2p(n, Bp, !uniform);
@@ -413,7 +417,7 @@ void plan_build(psa_plan* p, const psa_objective* f, const psa_engine_config* cf
             const long long pair_threads = static_cast<long long>(per_sm_p) * Bp * lim.sms;
             const long long pairs = (static_cast<long long>(p->chains_local) + 1) / 2;
             const bool worth = per_sm_p * Bp >= 256 && pairs >= pair_threads;
-            if (worth || mode == "pair") {
+            if (worth || mode == "pair" || mode == "lazypair") {
                 p->pair = true;
                 p->block = B = Bp;
                 p->smem = smem_p;
@@ -979,6 +983,7 @@ psa_status psa_plan_describe(const psa_plan* p, char* buf, int32_t capacity) {
                                                : p->pair       ? "v1_pair_kernel (two chains per thread, shared-memory pair rows)"
                                                : p->hbm_rows ? "v1_kernel (HBM SoA rows)"
                                                              : "v1_kernel (shared-memory rows)")
+                             : p->lazy && p->pair ? "v2_lazy_pair_kernel (deferred fold, two chains per thread, shared-memory pair rows)"
                              : p->pair     ? "v2_pair_kernel (two chains per thread, shared-memory pair rows)"
                              : p->pc       ? "v2_pc_kernel (producer/consumer warps, 32 chains per block)"
                              : p->lazy     ? (p->hbm_rows ? "v2_lazy_kernel (deferred fold, HBM SoA rows)"

@@ -337,6 +337,10 @@ struct Box {
     PSA_DEV double wd(int d) const { return uniform ? w0 : width[d]; }
     // compute_neighbour, sa_core.cpp:40-42: lower[d] + u*width(d) (mul, then add)
     PSA_DEV double point(int d, double u) const { return lo(d) + u * wd(d); }
+    // UB: the box is known to be uniform at compile time (no per-coordinate
+    // bound loads in the hot loop)
+    template <bool UB>
+    PSA_DEV double point_t(int d, double u) const { return UB ? lo0 + u * w0 : point(d, u); }
 };
 
 // ---------------------------------------------------------------------------
@@ -521,7 +525,7 @@ constexpr unsigned kFullWarp = 0xffffffffu;
 // idle lanes on a duplicate chain with mask == nullptr and a scratch
 // SweepStats), so its votes take the full mask: no divergence checks.
 
-template <class R, class Cost, int NT = 0, class Row = R*>
+template <class R, class Cost, int NT = 0, class Row = R*, bool UB = false>
 PSA_DEV R sweep_lazy(Row row, int n_rt, int family, R E, double temperature, uint32_t chain, uint32_t level,
                      uint32_t ctr, int N, const Box& box, const PhiloxKeys& keys, uint32_t* mask,
                      size_t mask_stride, double* x, size_t x_stride, SweepStats& st, R rr, R alpha) {
@@ -543,7 +547,7 @@ PSA_DEV R sweep_lazy(Row row, int n_rt, int family, R E, double temperature, uin
         const uint64_t m2 = draw_bits53_fast(ctr + 1, pc, keys);
         m3 = draw_bits53_fast(ctr + 2, pc, keys);
         d = min(static_cast<int>(static_cast<double>(m1) * idx_scale), n - 1);
-        xnew = box.point(d, bits_to_uniform(m2));
+        xnew = box.point_t<UB>(d, bits_to_uniform(m2));
         Cost::cache(static_cast<R>(xnew), d, n, tn);
         q1 = draw_bits53_fast(ctr + 3, pc, keys);
         q2 = draw_bits53_fast(ctr + 4, pc, keys);
@@ -556,7 +560,7 @@ PSA_DEV R sweep_lazy(Row row, int n_rt, int family, R E, double temperature, uin
         for (int j = 0; j < jn; ++j) {
             const R to = row[d];
             const int dn = min(static_cast<int>(static_cast<double>(q1) * idx_scale), n - 1);
-            const double xn = box.point(dn, bits_to_uniform(q2));
+            const double xn = box.point_t<UB>(dn, bits_to_uniform(q2));
             R tnn[1];
             bool ok;
             Cost::cache_common(static_cast<R>(xn), dn, n, tnn, ok);
@@ -601,8 +605,8 @@ PSA_DEV R sweep_lazy(Row row, int n_rt, int family, R E, double temperature, uin
                 have = false;
             }
             ctr += 3;
+            word |= static_cast<uint32_t>(r) << j; // r is 0 or 1 here
             if (r) {
-                word |= 1u << j;
                 if (x) x[static_cast<size_t>(d) * x_stride] = xnew;
             }
             d = dn;
@@ -806,6 +810,128 @@ PSA_DEV void sweep_pair(float* row, int n_rt, float& EA, float& EB, double tempe
         maskA[static_cast<size_t>(j0 >> 5) * mask_stride] = wordA;
         maskB[static_cast<size_t>(j0 >> 5) * mask_stride] = wordB;
     }
+    }
+}
+
+// Deferred fold for a chain pair (binary32 affine families): sweep_lazy's
+// interval decisions for two chains per thread, on a pair row (element k =
+// (t_k of A, t_k of B)), so the rare exact folds of both chains are one
+// FADD2 fold (pair_energy) and the loop, constants and mask words are shared
+// by two chains.  Called by all 32 lanes of a warp together.
+template <template <class> class F, int NT>
+PSA_DEV void sweep_lazy_pair(float* row, int n_rt, float& EA, float& EB, double temperature, uint32_t cA,
+                             uint32_t cB, uint32_t level, uint32_t ctr, int N, const Box& box,
+                             const PhiloxKeys& keys, uint32_t* maskA, uint32_t* maskB, size_t mask_stride,
+                             SweepStats& st, float rr, float alpha, bool cntA, bool cntB) {
+    using Fam = F<float>;
+    using Cost = SepCost<float, F>;
+    using L = LazyOf<Fam>;
+    static_assert(Fam::kArrays == 1, "deferred fold: one accumulator");
+    const int n = NT > 0 ? NT : n_rt;
+    const float k2 = metropolis_k2(temperature);
+    const PhiloxChain pa = philox_chain(cA, level, keys);
+    const PhiloxChain pb = philox_chain(cB, level, keys);
+    const double idx_scale = static_cast<double>(n) * 0x1.0p-53;
+    const float sa = L::sigma > 0 ? alpha : -alpha;
+    bool haveA = true, haveB = true;
+    int dA, dB;
+    float tA, tB;
+    {
+        const uint64_t a1 = draw_bits53_fast(ctr, pa, keys), a2 = draw_bits53_fast(ctr + 1, pa, keys);
+        const uint64_t b1 = draw_bits53_fast(ctr, pb, keys), b2 = draw_bits53_fast(ctr + 1, pb, keys);
+        dA = min(static_cast<int>(static_cast<double>(a1) * idx_scale), n - 1);
+        dB = min(static_cast<int>(static_cast<double>(b1) * idx_scale), n - 1);
+        float t[1];
+        Cost::cache(static_cast<float>(box.point(dA, bits_to_uniform(a2))), dA, n, t);
+        tA = t[0];
+        Cost::cache(static_cast<float>(box.point(dB, bits_to_uniform(b2))), dB, n, t);
+        tB = t[0];
+    }
+    for (int j0 = 0; j0 < N; j0 += 32) {
+        const int jn = N - j0 < 32 ? N - j0 : 32;
+        uint32_t wordA = 0, wordB = 0;
+        for (int j = 0; j < jn; ++j) {
+            const float oA = row[2 * dA], oB = row[2 * dB + 1];
+            // independent of this trial's outcome: its acceptance draws and
+            // the next proposals
+            const uint64_t mA = draw_bits53_fast(ctr + 2, pa, keys);
+            const uint64_t mB = draw_bits53_fast(ctr + 2, pb, keys);
+            const uint64_t a1 = draw_bits53_fast(ctr + 3, pa, keys), a2 = draw_bits53_fast(ctr + 4, pa, keys);
+            const uint64_t b1 = draw_bits53_fast(ctr + 3, pb, keys), b2 = draw_bits53_fast(ctr + 4, pb, keys);
+            const int nA = min(static_cast<int>(static_cast<double>(a1) * idx_scale), n - 1);
+            const int nB = min(static_cast<int>(static_cast<double>(b1) * idx_scale), n - 1);
+            const double yA = box.point(nA, bits_to_uniform(a2));
+            const double yB = box.point(nB, bits_to_uniform(b2));
+            float uA[1], uB[1];
+            bool okA, okB;
+            Cost::cache_common(static_cast<float>(yA), nA, n, uA, okA);
+            Cost::cache_common(static_cast<float>(yB), nB, n, uB, okB);
+            const MBand bA = metropolis_band(mA), bB = metropolis_band(mB);
+            // the interval decisions
+            const float qA = (tA - oA) * sa, qB = (tB - oB) * sa;
+            const float hA = qA + rr, lA = qA - rr, hB = qB + rr, lB = qB - rr;
+            int rA = ((hA <= 0.0f) | (hA * k2 < bA.lo)) ? 1 : (((lA > 0.0f) & (lA * k2 > bA.hi)) ? 0 : -1);
+            int rB = ((hB <= 0.0f) | (hB * k2 < bB.lo)) ? 1 : (((lB > 0.0f) & (lB * k2 > bB.hi)) ? 0 : -1);
+            bool setA = false, setB = false;
+            if (__any_sync(kFullWarp, (!(okA & okB)) | (rA < 0) | (rB < 0))) {
+                if (!okA) Cost::cache(static_cast<float>(yA), nA, n, uA);
+                if (!okB) Cost::cache(static_cast<float>(yB), nB, n, uB);
+                if (__any_sync(kFullWarp, (rA < 0) | (rB < 0))) {
+                    if (__any_sync(kFullWarp, ((rA < 0) & !haveA) | ((rB < 0) & !haveB))) {
+                        float eA, eB;
+                        pair_energy<Fam, NT>(row, n, eA, eB);
+                        if (!haveA) EA = eA;
+                        if (!haveB) EB = eB;
+                        haveA = haveB = true;
+                    }
+                    if (rA < 0) row[2 * dA] = tA;
+                    if (rB < 0) row[2 * dB + 1] = tB;
+                    float eA, eB;
+                    pair_energy<Fam, NT>(row, n, eA, eB);
+                    if (rA < 0) {
+                        int v = metropolis_fast<float>(eA, EA, k2, bA);
+                        if (v < 0) v = Accept<float>::exact(static_cast<double>(eA) - static_cast<double>(EA), temperature, mA);
+                        if (v) EA = eA;
+                        else row[2 * dA] = oA;
+                        rA = v;
+                        setA = true;
+                        st.settles += cntA;
+                    }
+                    if (rB < 0) {
+                        int v = metropolis_fast<float>(eB, EB, k2, bB);
+                        if (v < 0) v = Accept<float>::exact(static_cast<double>(eB) - static_cast<double>(EB), temperature, mB);
+                        if (v) EB = eB;
+                        else row[2 * dB + 1] = oB;
+                        rB = v;
+                        setB = true;
+                        st.settles += cntB;
+                    }
+                }
+            }
+            if (rA && !setA) {
+                row[2 * dA] = tA;
+                haveA = false;
+            }
+            if (rB && !setB) {
+                row[2 * dB + 1] = tB;
+                haveB = false;
+            }
+            ctr += 3;
+            wordA |= static_cast<uint32_t>(rA) << j;
+            wordB |= static_cast<uint32_t>(rB) << j;
+            dA = nA;
+            dB = nB;
+            tA = uA[0];
+            tB = uB[0];
+        }
+        if (maskA) maskA[static_cast<size_t>(j0 >> 5) * mask_stride] = wordA;
+        if (maskB) maskB[static_cast<size_t>(j0 >> 5) * mask_stride] = wordB;
+    }
+    if (__any_sync(kFullWarp, !(haveA & haveB))) {
+        float eA, eB;
+        pair_energy<Fam, NT>(row, n, eA, eB);
+        if (!haveA) EA = eA;
+        if (!haveB) EB = eB;
     }
 }
 

@@ -407,8 +407,28 @@ struct PairOf<SepCost<float, F>> {
     }
 };
 
+// deferred-fold capability of a cost (SepCost of a LazyOf family)
+template <class Cost>
+struct LazyCost {
+    static constexpr bool value = false;
+};
+template <class R, template <class> class F>
+struct LazyCost<SepCost<R, F>> {
+    static constexpr bool value = LazyOf<F<R>>::value;
+    template <class T>
+    using Fam = F<T>;
+    static double radius(int n, const double* lo, const double* hi) {
+        if constexpr (LazyOf<F<R>>::value) return lazy_radius<R, F>(n, lo, hi);
+        else return -1.0;
+    }
+    static double alpha(int n) {
+        if constexpr (LazyOf<F<R>>::value) return LazyOf<F<R>>::alpha(n);
+        else return 0.0;
+    }
+};
+
 // LZ: the deferred-fold sweep (sweep_lazy; Cost = SepCost of a LazyOf family)
-template <class R, class Cost, int NT, bool G, bool PAIR, bool PC = false, bool LZ = false>
+template <class R, class Cost, int NT, bool G, bool PAIR, bool PC = false, bool LZ = false, bool UB = false>
 __device__ __forceinline__ void v2_body(const EngineArgs& a) {
     constexpr int A = Cost::A;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -504,6 +524,78 @@ __device__ __forceinline__ void v2_body(const EngineArgs& a) {
                     if (better(mine, best)) best = mine;
                 }
             }
+        } else if constexpr (PAIR && LZ) {
+            // deferred fold on chain pairs: a warp takes 64 chains of the
+            // level at a time (dynamic assignment, as in the one-chain
+            // kernel below): lane l runs chains base + l (A) and base + 32 + l
+            // (B); idle halves sweep a duplicate of chain `base` (identical
+            // bits, nothing recorded; sweep_pair's mask words for it are the
+            // live lane's own values)
+            const bool fold_mode = sh->fold_mode;
+            const uint64_t settles0 = st.settles;
+            unsigned long long my_chains = 0;
+            if (blockIdx.x == 0 && tid == 0) a.work[(l + 1) & 1] = 0;
+            unsigned long long* wc = a.work + (l & 1);
+            const int lane = tid & 31;
+            float* prow = reinterpret_cast<float*>(row);
+            for (;;) {
+                unsigned long long base = 0;
+                if (lane == 0) base = atomicAdd(wc, 64ull);
+                base = __shfl_sync(0xffffffffu, base, 0);
+                if (base >= a.chains_local) break;
+                const bool vA = base + lane < a.chains_local, vB = base + 32 + lane < a.chains_local;
+                const size_t clA = vA ? base + lane : base, clB = vB ? base + 32 + lane : base;
+                const uint32_t cA = static_cast<uint32_t>(a.chain_begin + clA);
+                const uint32_t cB = static_cast<uint32_t>(a.chain_begin + clB);
+                float eA, eB;
+                uint32_t ctr = 0;
+                if (l == 0 && a.random_start) {
+                    for (int k = 0; k < n; ++k) {
+                        float ta[A], tb[A];
+                        Cost::cache(static_cast<float>(random_start_coord(a, box, cA, k)), k, n, ta);
+                        Cost::cache(static_cast<float>(random_start_coord(a, box, cB, k)), k, n, tb);
+#pragma unroll
+                        for (int q = 0; q < A; ++q) {
+                            prow[2 * (k * A + q)] = ta[q];
+                            prow[2 * (k * A + q) + 1] = tb[q];
+                        }
+                    }
+                    PairOf<Cost>::template energy<NT>(prow, n, eA, eB);
+                    ctr = static_cast<uint32_t>(n);
+                    st.draws += static_cast<uint64_t>(n) * (vA + vB);
+                    const Cand s1 = start_cand(static_cast<double>(eA), static_cast<int32_t>(cA));
+                    if (vA && better(s1, sbest)) sbest = s1;
+                    const Cand s2 = start_cand(static_cast<double>(eB), static_cast<int32_t>(cB));
+                    if (vB && better(s2, sbest)) sbest = s2;
+                } else {
+                    unsigned long long* u = reinterpret_cast<unsigned long long*>(prow);
+                    const float* vf = reinterpret_cast<const float*>(vs);
+                    for (int e = 0; e < n * A; ++e) u[e] = f2_make(vf[e], vf[e]).v;
+                    eA = eB = static_cast<float>(estar);
+                }
+                if (l == 0) st.evals += vA + vB; // the start evaluations (engines.cpp:157)
+                if (!fold_mode) {
+                    if constexpr (LazyCost<Cost>::value)
+                        sweep_lazy_pair<LazyCost<Cost>::template Fam, NT>(
+                            prow, n, eA, eB, temperature, cA, cB, static_cast<uint32_t>(l), ctr, a.N, box, a.keys,
+                            vA ? masks + clA : nullptr, vB ? masks + clB : nullptr, a.mask_stride, st,
+                            static_cast<float>(a.lazy_r), static_cast<float>(a.lazy_alpha), vA, vB);
+                    my_chains += vA + vB;
+                } else {
+                    PairOf<Cost>::template run<NT>(prow, n, eA, eB, temperature, cA, cB, static_cast<uint32_t>(l), ctr,
+                                                   a.N, box, a.keys, masks + clA, masks + clB, a.mask_stride);
+                }
+                st.evals += static_cast<uint64_t>(a.N) * (vA + vB);
+                st.draws += 3ull * static_cast<uint64_t>(a.N) * (vA + vB);
+                const Cand m1{static_cast<double>(eA), static_cast<int32_t>(cA), 0};
+                if (vA && better(m1, best)) best = m1;
+                const Cand m2{static_cast<double>(eB), static_cast<int32_t>(cB), 0};
+                if (vB && better(m2, best)) best = m2;
+            }
+            if (!fold_mode) {
+                atomicAdd(&sh->lv_settles, static_cast<unsigned long long>(st.settles - settles0));
+                atomicAdd(&sh->lv_chains, my_chains);
+            }
         } else if constexpr (PAIR) {
             // pair p = chains p and p + P (P = ceil(C/2)); an odd count leaves
             // the last pair's chain B a duplicate whose results are dropped
@@ -588,7 +680,8 @@ __device__ __forceinline__ void v2_body(const EngineArgs& a) {
             if constexpr (LZ) lazy = !fold_mode;
             if (lazy) {
                 if constexpr (LZ)
-                    e = sweep_lazy<R, Cost, NT>(row, n, a.family, e, temperature, c, static_cast<uint32_t>(l), ctr,
+                    e = sweep_lazy<R, Cost, NT, decltype(row), UB>(row, n, a.family, e, temperature, c,
+                                                                   static_cast<uint32_t>(l), ctr,
                                                 a.N, box, a.keys, live ? masks + cl : nullptr, a.mask_stride,
                                                 nullptr, 0, st, static_cast<R>(a.lazy_r),
                                                 static_cast<R>(a.lazy_alpha));
@@ -725,10 +818,17 @@ __global__ void __launch_bounds__(PSA_V2_MAX_THREADS, PSA_V2_MIN_BLOCKS) v2_kern
     v2_body<R, Cost, NT, G, false>(a);
 }
 
-// deferred fold (sweep_lazy): one chain per thread, rows in shared memory or HBM
-template <class R, class Cost, int NT, bool G>
+// deferred fold on chain pairs (sweep_lazy_pair), shared-memory pair rows
+template <class R, class Cost, int NT>
+__global__ void __launch_bounds__(128, 2) v2_lazy_pair_kernel(const EngineArgs a) {
+    v2_body<R, Cost, NT, false, true, false, true>(a);
+}
+
+// deferred fold (sweep_lazy): one chain per thread, rows in shared memory or
+// HBM; UB: uniform box (the benchmark shapes), resolved at compile time
+template <class R, class Cost, int NT, bool G, bool UB = false>
 __global__ void __launch_bounds__(PSA_V2_MAX_THREADS, PSA_V2_MIN_BLOCKS) v2_lazy_kernel(const EngineArgs a) {
-    v2_body<R, Cost, NT, G, false, false, true>(a);
+    v2_body<R, Cost, NT, G, false, false, true, UB>(a);
 }
 
 // producer/consumer blocks for small chain counts: warp 0 consumes, warps
@@ -1252,24 +1352,6 @@ __global__ void sweep_one(const EngineArgs a, double* x, R* row, double* energy,
 // Host-side dispatch over (precision, family)
 // ---------------------------------------------------------------------------
 
-// deferred-fold capability of a cost (SepCost of a LazyOf family)
-template <class Cost>
-struct LazyCost {
-    static constexpr bool value = false;
-};
-template <class R, template <class> class F>
-struct LazyCost<SepCost<R, F>> {
-    static constexpr bool value = LazyOf<F<R>>::value;
-    static double radius(int n, const double* lo, const double* hi) {
-        if constexpr (LazyOf<F<R>>::value) return lazy_radius<R, F>(n, lo, hi);
-        else return -1.0;
-    }
-    static double alpha(int n) {
-        if constexpr (LazyOf<F<R>>::value) return LazyOf<F<R>>::alpha(n);
-        else return 0.0;
-    }
-};
-
 template <class R, class Cost, int NT = 0>
 struct KernelSet {
     static EngineKernels get() {
@@ -1293,14 +1375,18 @@ struct KernelSet {
             return engine_smem_bytes<R, Cost::A>(n, 32, box, true) + 16 + sizeof(PcEntry<R, Cost::A>) * 3 * 32 * 32;
         };
         k.v2z = nullptr;
+        k.v2zu = nullptr;
         k.v2gz = nullptr;
+        k.v2pz = nullptr;
         k.lazy_radius = nullptr;
         k.lazy_alpha_of = nullptr;
         if constexpr (LazyCost<Cost>::value) {
             k.v2z = reinterpret_cast<const void*>(&v2_lazy_kernel<R, Cost, NT, false>);
+            k.v2zu = reinterpret_cast<const void*>(&v2_lazy_kernel<R, Cost, NT, false, true>);
             k.v2gz = reinterpret_cast<const void*>(&v2_lazy_kernel<R, Cost, 0, true>);
             k.lazy_radius = &LazyCost<Cost>::radius;
             k.lazy_alpha_of = &LazyCost<Cost>::alpha;
+            if constexpr (PairOf<Cost>::value) k.v2pz = reinterpret_cast<const void*>(&v2_lazy_pair_kernel<R, Cost, NT>);
         }
         if constexpr (PairOf<Cost>::value) {
             k.v1p = reinterpret_cast<const void*>(&v1_pair_kernel<R, Cost, NT>);

@@ -62,7 +62,7 @@ def device(gpu_lib, engine, family, dim, chains, sched, prec):
     return as_golden(res.as_dict())
 
 
-@pytest.mark.parametrize("mode", ["", "single", "pair"])
+@pytest.mark.parametrize("mode", ["", "single", "pair", "lazy1"])
 @pytest.mark.parametrize("key", ["f32", "f64"])
 def test_c2_full_chain_count_bitwise_vs_reference(gpu_lib, bench_golden, monkeypatch, key, mode):
     rec = bench_golden[f"c2_{key}"]

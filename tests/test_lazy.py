@@ -23,11 +23,12 @@ from test_gpu_parity import device_run
 
 pytestmark = pytest.mark.gpu
 
-@pytest.fixture(autouse=True)
-def _lazy_kernel(monkeypatch):
+@pytest.fixture(autouse=True, params=["lazy1", "lazypair"])
+def _lazy_kernel(request, monkeypatch):
     """small chain counts default to the producer/consumer kernel; these
-    tests pin the deferred-fold one"""
-    monkeypatch.setenv("PSA_V2_MODE", "lazy")
+    tests pin the deferred-fold kernels: one chain per thread (lazy1) and
+    chain pairs (lazypair; binary32 only — f64 plans fall back to lazy1)"""
+    monkeypatch.setenv("PSA_V2_MODE", request.param)
 
 
 LAZY = [("SCHWEFEL", -512.0, 512.0), ("RASTRIGIN", -5.12, 5.12), ("SPHERE", -2.0, 2.0),
@@ -53,7 +54,8 @@ def test_lazy_matches_oracle(gpu_lib, family, lo, hi, prec, dim):
         assert not same_run(got, want), (family, dim, prec, start, same_run(got, want))
 
 
-def test_lazy_kernel_is_the_default_for_affine_families(gpu_lib):
+def test_lazy_kernel_is_the_default_for_affine_families(gpu_lib, monkeypatch):
+    monkeypatch.delenv("PSA_V2_MODE", raising=False)
     d = _plan_desc("SCHWEFEL", 100, -512.0, 512.0, 1 << 16, (1000.0, 989.01, 0.99, 100),
                    psa.Precision.f32)
     assert d.startswith("v2_lazy_kernel"), d
