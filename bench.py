@@ -12,7 +12,9 @@ rho=0.99, N=100 (1146 levels), precision f32 (the paper's default).  One
              already resident in HBM (psa_plan_launch)
   e2e        the same metric through the public C-ABI call with host buffers
              (psa_run_synchronous: problem upload, launch, result download)
-  roofline   the engine kernel against the SM issue roofline
+  roofline   the engine kernel against its binding resource: the
+             integer-multiply pipe for the deferred-fold kernel (Philox
+             mulhilo per trial / measured IMAD.WIDE rate)
   cpu_baseline  the reference's own CPU implementation (oracle/_ref, all host
              threads) on a bounded sample of the same workload
 
@@ -196,11 +198,52 @@ def run_reference_arm(args):
 ARRAYS = {"F0_a": 1, "F1_a": 2, "F13_a": 1}
 
 
-def _smem_peak():
+def _simt_peaks():
+    """measured on this pool's B200 by scripts/simt_peaks.cu (profiles/simt_peaks.json)"""
     try:
-        return float(json.load(open(os.path.join(ROOT, "profiles", "simt_peaks.json")))["smem_bytes_per_s"])
+        pk = json.load(open(os.path.join(ROOT, "profiles", "simt_peaks.json")))
+        return (float(pk["smem_bytes_per_s"]), float(pk["imad_wide_lane_ops_per_s"]),
+                "measured: profiles/simt_peaks.json (scripts/simt_peaks.cu)")
     except (OSError, KeyError, ValueError):
-        return 148 * 128 * 1.965e9
+        return 148 * 128 * 1.965e9, 148 * 32 * 1.965e9, "nominal (148 SMs x 1.965 GHz; 128 B/clk smem, 32 IMAD.WIDE lanes/clk)"
+
+
+def _smem_peak():
+    return _simt_peaks()[0]
+
+
+# The Philox4x32-10 stream of the reference (rng.hpp:39-76): one block per
+# draw, three draws per trial.  A block is 10 rounds of two 32x32->64
+# multiplies; for a fixed (chain, level) the chain and level words make the
+# first-round product of word 2 and the second-round product of word 0
+# invariants, and the last round needs one product only: 17 mulhilo per
+# draw, 51 per trial (philox.cuh, draw_bits53_fast).
+PHILOX_MULHILO_PER_TRIAL = 51
+
+
+def kernel_roofline(desc, dim, bytes_per_coord, trials, seconds):
+    """Roofline of one engine launch by kernel kind (Roofline).
+
+    * deferred-fold kernels (v2_lazy*): a trial reads two cached terms and
+      folds only when its energy interval straddles the Metropolis band, so
+      the binding resource is the integer-multiply (fma-heavy) pipe running
+      the reference's Philox stream: 51 IMAD.WIDE-equivalent mulhilo per
+      trial against the measured IMAD.WIDE.U32 rate;
+    * fold-every-trial kernels: shared-memory bandwidth, bytes_per_coord*n
+      bytes of cached terms read by each trial's sequential fold."""
+    smem_peak, imad_peak, src = _simt_peaks()
+    rate = trials / seconds
+    if desc.startswith("v2_lazy"):
+        ach = rate * PHILOX_MULHILO_PER_TRIAL
+        return {"bound": "imad", "achieved": ach / 1e12, "peak": imad_peak / 1e12, "unit": "T mulhilo/s",
+                "frac": ach / imad_peak, "algorithmic_ops_per_trial": PHILOX_MULHILO_PER_TRIAL,
+                "algorithmic_unit": "32x32->64 multiplies (Philox4x32-10, 3 draws per trial)",
+                "peak_source": src + ", IMAD.WIDE.U32 stream",
+                "fold_bytes_per_trial_if_folded": bytes_per_coord * dim}
+    bpt = bytes_per_coord * dim
+    bw = rate * bpt
+    return {"bound": "smem", "achieved": bw / 1e9, "peak": smem_peak / 1e9, "unit": "GB/s", "frac": bw / smem_peak,
+            "algorithmic_bytes_per_trial": bpt, "peak_source": src + ", LDS.128 stream"}
 
 
 def _time_plan(psa, torch, f, cfg, engine, flush, reps):
@@ -230,21 +273,18 @@ def measure_configs(psa, torch, flush):
     with its kernel and its fraction of the shared-memory roofline; plus the
     C4 Nelder-Mead phase (per-iteration time at n=500 from the SA best)."""
     paper = psa.AnnealSchedule(1000.0, 0.01, 0.99, 100)
-    peak = _smem_peak()
     out = []
 
     def entry(cname, workload, fid, f, cfg, engine, reps):
         r, ms, desc, launches = _time_plan(psa, torch, f, cfg, engine, flush, reps)
         assert r.evaluations == psa.expected_evaluations(cfg.schedule, cfg.n_chains)
         trials = r.evaluations - cfg.n_chains
-        bpt = (4 if cfg.precision == psa.Precision.f32 else 8) * ARRAYS[fid] * f.dim
-        bw = trials * bpt / (ms / 1e3)
+        bpc = (4 if cfg.precision == psa.Precision.f32 else 8) * ARRAYS[fid]
         out.append({"config": cname, "workload": workload, "engine": {1: "v1", 2: "v2"}[engine],
                     "function": fid, "n": f.dim, "chains": cfg.n_chains, "levels": len(r.trace),
                     "dtype": cfg.precision.name, "evaluations": r.evaluations, "ms": ms,
                     "value": r.evaluations / (ms / 1e3), "unit": UNIT, "kernel": desc, "launches": launches,
-                    "roofline": {"bound": "smem", "algorithmic_bytes_per_trial": bpt, "achieved": bw / 1e9,
-                                 "peak": peak / 1e9, "unit": "GB/s", "frac": bw / peak},
+                    "roofline": kernel_roofline(desc, f.dim, bpc, trials, ms / 1e3),
                     "best_f": r.best_f, "winning_chain": r.winning_chain})
         return r
 
@@ -419,34 +459,27 @@ def main():
     h2d = 8 * (3 * N_DIM + levels) + 256  # bounds, widths, start, ladder, kernel args
     d2h = 8 * (N_DIM + levels) + 32       # best_x, trace, scalars
 
-    # Roofline of the engine kernel ("Roofline"): the binding
-    # resource of the term-cached sweep is shared-memory bandwidth — every
-    # trial's sequential fold must read the chain's n cached terms (4n bytes
-    # in f32, 8n in f64) from its shared-memory row.  Peak: the LDS.128
-    # bandwidth measured on this pool's B200 by scripts/simt_peaks.cu.
+    # Roofline of the engine kernel ("Roofline"): by kernel kind
+    # (kernel_roofline): the deferred-fold kernel is bound by the integer-
+    # multiply pipe (the reference's Philox stream), the fold-every-trial
+    # kernels by shared-memory bandwidth.  Peaks measured on this pool's B200
+    # (profiles/simt_peaks.json).
     sm_count = torch.cuda.get_device_properties(local).multi_processor_count
-    peaks_path = os.path.join(ROOT, "profiles", "simt_peaks.json")
-    smem_peak = sm_count * 128 * 1.965e9  # nominal 128 B/clk/SM at max clock
-    peak_src = "nominal 128 B/clk/SM x 148 SMs x 1.965 GHz"
-    if os.path.exists(peaks_path):
-        try:
-            smem_peak = float(json.load(open(peaks_path))["smem_bytes_per_s"])
-            peak_src = "measured: profiles/simt_peaks.json (scripts/simt_peaks.cu, LDS.128 stream)"
-        except (OSError, KeyError, ValueError):
-            pass
-    term_bytes = (4 if args.precision == "f32" else 8) * N_DIM
     trials_local = chains_per_gpu * SCHEDULE[3] * levels
     kernel_s = local_ms / args.steps / 1e3
-    achieved_bw = trials_local * term_bytes / kernel_s
-    ncu_path = os.path.join(ROOT, "profiles", "r01_v2_f32_ncu.json")
+    roof = kernel_roofline(plan.description, N_DIM, 4 if args.precision == "f32" else 8, trials_local, kernel_s)
+    lazy = plan.description.startswith("v2_lazy")
+    ncu_path = os.path.join(ROOT, "profiles", "r02_v2_lazy_f32_ncu.json" if lazy else "r01_v2_f32_ncu.json")
     traffic = None
     issue_frac = None
+    fmaheavy = None
     if os.path.exists(ncu_path):
         try:
             nj = json.load(open(ncu_path))
             # DRAM bytes per trial in the profiled launch, scaled to this launch
             traffic = nj["dram_bytes_per_trial"] * trials_local
             issue_frac = nj["issue_active_frac"]
+            fmaheavy = nj.get("pipe_fmaheavy_pct")
         except (OSError, KeyError, ValueError):
             pass
     sfu_roof = sm_count * 16 * 1.965e9 / (2 * N_DIM + 1)
@@ -468,17 +501,14 @@ def main():
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "api": "psa_run_synchronous (C-ABI, host buffers)", "ms_per_call": e2e_ms, "clocks": e2e_clocks},
         "gpu_launches": args.steps * plan.launches_per_run,
-        "roofline": {"bound": "smem", "achieved": achieved_bw / 1e9, "peak": smem_peak / 1e9, "unit": "GB/s",
-                     "frac": achieved_bw / smem_peak, "traffic": traffic,
-                     "kernel": plan.description + " (persistent cooperative)",
-                     "algorithmic_bytes_per_trial": term_bytes, "trials_per_launch": trials_local,
-                     "kernel_ms": kernel_s * 1e3, "peak_source": peak_src,
-                     "traffic_note": "DRAM bytes (ncu, profiles/r01_v2_f32_ncu.json) scaled to this launch; "
-                                     "state is on-chip, so DRAM traffic is ~0",
-                     "issue_active_frac_ncu": issue_frac,
-                     "trials_per_s": trials_local / kernel_s,
-                     "sfu_full_eval_roofline_trials_per_s": sfu_roof,
-                     "trials_per_s_vs_sfu_full_eval_roofline": (trials_local / kernel_s) / sfu_roof},
+        "roofline": dict(roof, traffic=traffic, kernel=plan.description + " (persistent cooperative)",
+                         trials_per_launch=trials_local, kernel_ms=kernel_s * 1e3,
+                         traffic_note=f"DRAM bytes (ncu, profiles/{os.path.basename(ncu_path)}) scaled to this "
+                                      "launch; chain state is on-chip, so DRAM traffic is ~0",
+                         issue_active_frac_ncu=issue_frac, fmaheavy_pipe_pct_ncu=fmaheavy,
+                         trials_per_s=trials_local / kernel_s,
+                         sfu_full_eval_roofline_trials_per_s=sfu_roof,
+                         trials_per_s_vs_sfu_full_eval_roofline=(trials_local / kernel_s) / sfu_roof),
         "clocks": clocks,
         "result": {"best_f": res.best_f, "winning_chain": res.winning_chain, "evaluations": res.evaluations},
     }

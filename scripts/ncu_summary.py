@@ -83,6 +83,7 @@ def main():
         "pipe_fma_pct": f("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"),
         "pipe_alu_pct": f("sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active"),
         "pipe_fp64_pct": f("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
+        "pipe_fmaheavy_pct": f("sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed"),
         "pipe_xu_pct": f("sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active"),
         "pipe_lsu_pct": f("sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active"),
         "instructions_per_warp_trial": sum(ops.values()),
@@ -98,7 +99,7 @@ def main():
         fh.write("| metric | value |\n|---|---|\n")
         for k in ("duration_ms", "trials", "trials_per_s", "dram_bytes", "dram_bytes_per_trial", "issue_active_frac",
                   "smem_wavefronts", "smem_bank_conflicts", "registers_per_thread", "warps_active_per_sm",
-                  "pipe_fma_pct", "pipe_alu_pct", "pipe_fp64_pct", "pipe_xu_pct", "pipe_lsu_pct",
+                  "pipe_fma_pct", "pipe_fmaheavy_pct", "pipe_alu_pct", "pipe_fp64_pct", "pipe_xu_pct", "pipe_lsu_pct",
                   "instructions_per_warp_trial"):
             fh.write(f"| {k} | {summary[k]:.6g} |\n")
         fh.write("\n## Stall reasons (warps stalled per issued instruction)\n\n")
