@@ -343,12 +343,12 @@ void plan_build(psa_plan* p, const psa_objective* f, const psa_engine_config* cf
     // chain rows resident per SM (large rows: three 32-thread blocks hold
     // more rows than one 64-thread block); ties go to the larger block
     auto kern_of = [&](bool g) {
-        if (p->lazy) return g ? p->ks.v2gz : uniform ? p->ks.v2zu : p->ks.v2z;
+        if (p->lazy) return g ? (uniform ? p->ks.v2gzu : p->ks.v2gz) : uniform ? p->ks.v2zu : p->ks.v2z;
         return engine == 1 ? (g ? p->ks.v1g : p->ks.v1) : (g ? p->ks.v2g : p->ks.v2);
     };
     int B = 32;
+    int best = -1; // chain rows resident per SM with shared-memory rows
     {
-        int best = -1;
         for (int cand : {128, 96, 64, 32}) {
             const size_t sm_b = smem_of(cand);
             if (sm_b > smem_cap) continue;
@@ -368,7 +368,25 @@ void plan_build(psa_plan* p, const psa_objective* f, const psa_engine_config* cf
     // (PSA_FORCE_HBM_ROWS=1 selects it at any n: the parity tests compare the
     // two layouts bit for bit)
     const char* force = std::getenv("PSA_FORCE_HBM_ROWS");
-    p->hbm_rows = smem_of(B) > smem_cap || (force && force[0] == '1');
+    // The deferred fold touches a row once per trial (one term read, a write
+    // on acceptance) plus rare folds, so when shared-memory rows leave fewer
+    // than 8 warps per SM (large n: C4's n = 500 keeps 3) its rows go to HBM
+    // and the SM keeps its full complement of warps (PSA_FORCE_HBM_ROWS=0
+    // keeps them in shared memory).
+    // In binary32 at large n the interval is wide enough that low
+    // temperatures settle often (n = 500: 1.3% of trials at T = 1, each
+    // settle two n-term folds from HBM), so there HBM rows are used only
+    // when the ladder stays above rr * n (measured: settles <= 0.2% at
+    // n = 500 down to T ~ rr n / 1); binary64 intervals are ~1e-12 wide.
+    double lazy_rr = 0;
+    if (p->lazy) {
+        std::vector<double> upper(n);
+        for (int k = 0; k < n; ++k) upper[k] = f->lower[k] + width[k];
+        lazy_rr = p->ks.lazy_radius(n, f->lower, upper.data());
+    }
+    const bool warm = p->precision == PSA_F64 || p->temps.back() >= lazy_rr * n;
+    const bool lazy_hbm = p->lazy && best < 256 && warm && !(force && force[0] == '0');
+    p->hbm_rows = smem_of(B) > smem_cap || (force && force[0] == '1') || lazy_hbm;
     if (p->hbm_rows) {
         B = 128;
         if (p->ks.smem_g(n, B, !uniform) > smem_cap)
@@ -509,9 +527,7 @@ void plan_build(psa_plan* p, const psa_objective* f, const psa_engine_config* cf
     a.rank = p->rank;
     a.spin_limit = 60ll * 2000000000ll; // ~60 s at 2 GHz
     if (p->lazy) {
-        std::vector<double> upper(n);
-        for (int k = 0; k < n; ++k) upper[k] = f->lower[k] + width[k];
-        a.lazy_r = p->ks.lazy_radius(n, f->lower, upper.data());
+        a.lazy_r = lazy_rr;
         const char* adapt = std::getenv("PSA_LAZY_ADAPT"); // 0: never fall back (tests)
         a.lazy_adapt = !(adapt && adapt[0] == '0');
         a.lazy_alpha = p->ks.lazy_alpha_of(n);

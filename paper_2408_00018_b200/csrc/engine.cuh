@@ -553,13 +553,16 @@ PSA_DEV R sweep_lazy(Row row, int n_rt, int family, R E, double temperature, uin
         q2 = draw_bits53_fast(ctr + 4, pc, keys);
         q3 = draw_bits53_fast(ctr + 5, pc, keys);
     }
+    // the cached term a trial replaces is loaded one trial ahead (HBM rows:
+    // the load latency overlaps the previous trial)
+    R to = row[d];
     for (int j0 = 0; j0 < N; j0 += 32) {
         const int jn = N - j0 < 32 ? N - j0 : 32;
         uint32_t word = 0;
 #pragma unroll kLazyUnroll
         for (int j = 0; j < jn; ++j) {
-            const R to = row[d];
             const int dn = min(static_cast<int>(static_cast<double>(q1) * idx_scale), n - 1);
+            const R tp = row[dn]; // next trial's replaced term (fixed up below if this trial writes dn)
             const double xn = box.point_t<UB>(dn, bits_to_uniform(q2));
             R tnn[1];
             bool ok;
@@ -609,6 +612,7 @@ PSA_DEV R sweep_lazy(Row row, int n_rt, int family, R E, double temperature, uin
             if (r) {
                 if (x) x[static_cast<size_t>(d) * x_stride] = xnew;
             }
+            to = (r && dn == d) ? tn[0] : tp;
             d = dn;
             xnew = xn;
             m3 = q3;

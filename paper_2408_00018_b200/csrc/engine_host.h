@@ -147,6 +147,7 @@ struct EngineKernels {
     const void* v2z;  // shared-memory rows
     const void* v2zu; // shared-memory rows, uniform box
     const void* v2gz; // HBM rows
+    const void* v2gzu; // HBM rows, uniform box
     const void* v2pz; // chain pairs (binary32), shared-memory pair rows
     double (*lazy_radius)(int n, const double* lower, const double* upper);
     double (*lazy_alpha_of)(int n);

@@ -672,7 +672,21 @@ __device__ __forceinline__ void v2_body(const EngineArgs& a) {
                 const Cand s = start_cand(static_cast<double>(e), static_cast<int32_t>(c));
                 if (live && better(s, sbest)) sbest = s;
             } else {
-                for (int k = 0; k < n * A; ++k) row[k] = vs[k];
+                if constexpr (G) {
+                    // HBM rows: whole 16-byte vectors (a warp writes 512
+                    // contiguous bytes per store); the padding of the last
+                    // vector is never read
+                    using V = Vec16<R>;
+                    for (int q = 0; q < (n * A + V::W - 1) / V::W; ++q) {
+                        typename V::T v;
+                        R* pv = reinterpret_cast<R*>(&v);
+#pragma unroll
+                        for (int i = 0; i < V::W; ++i) pv[i] = q * V::W + i < n * A ? vs[q * V::W + i] : R(0);
+                        *reinterpret_cast<typename V::T*>(row.p + static_cast<size_t>(q) * row.s) = v;
+                    }
+                } else {
+                    for (int k = 0; k < n * A; ++k) row[k] = vs[k];
+                }
                 e = estar;
             }
             if (l == 0) st.evals += 1; // the start evaluation (engines.cpp:157)
@@ -1377,6 +1391,7 @@ struct KernelSet {
         k.v2z = nullptr;
         k.v2zu = nullptr;
         k.v2gz = nullptr;
+        k.v2gzu = nullptr;
         k.v2pz = nullptr;
         k.lazy_radius = nullptr;
         k.lazy_alpha_of = nullptr;
@@ -1384,6 +1399,7 @@ struct KernelSet {
             k.v2z = reinterpret_cast<const void*>(&v2_lazy_kernel<R, Cost, NT, false>);
             k.v2zu = reinterpret_cast<const void*>(&v2_lazy_kernel<R, Cost, NT, false, true>);
             k.v2gz = reinterpret_cast<const void*>(&v2_lazy_kernel<R, Cost, 0, true>);
+            k.v2gzu = reinterpret_cast<const void*>(&v2_lazy_kernel<R, Cost, 0, true, true>);
             k.lazy_radius = &LazyCost<Cost>::radius;
             k.lazy_alpha_of = &LazyCost<Cost>::alpha;
             if constexpr (PairOf<Cost>::value) k.v2pz = reinterpret_cast<const void*>(&v2_lazy_pair_kernel<R, Cost, NT>);

@@ -137,3 +137,32 @@ def test_metropolis_pretest_never_contradicts_the_exact_test(gpu_lib, prec):
     assert certain + undecided == 1 << 30
     assert wrong == 0, (certain, wrong, undecided)
     assert certain > (1 << 30) // 8  # the draws away from the boundary are settled by the band
+
+
+@pytest.mark.parametrize("prec", [0, 1])
+def test_large_n_lazy_hbm_rows_match_oracle(gpu_lib, prec):
+    """n = 500 (C4's SA phase): the deferred fold keeps its rows in HBM
+    (shared-memory rows would leave 3 warps per SM)."""
+    prob = Problem("SCHWEFEL", 500, -512.0, 512.0)
+    sched = (1000.0, 100.0, 0.5, 100)  # warm: binary32 keeps HBM rows only above rr * n
+    cfg = Config(64, sched, 8, prec, 1)
+    desc = _plan_desc("SCHWEFEL", 500, -512.0, 512.0, 64, sched, psa.Precision(prec))
+    assert desc.startswith("v2_lazy_kernel (deferred fold, HBM SoA rows)"), desc
+    got = device_run(2, prob, cfg)
+    want = oracle_sync(prob, cfg)
+    assert not same_run(got, want), same_run(got, want)
+
+
+@pytest.mark.parametrize("prec", [0, 1])
+def test_large_n_lazy_equals_fold_every_trial(gpu_lib, monkeypatch, prec):
+    """n = 500 at 40000 chains over the C4 schedule's first and a low-T
+    window: HBM-row deferred fold == fold-every-trial kernel, bitwise."""
+    monkeypatch.delenv("PSA_V2_MODE", raising=False)
+    prob = Problem("SCHWEFEL", 500, -512.0, 512.0)
+    for sched in ((1000.0, 700.0, 0.9, 100), (0.5, 0.2, 0.8, 100)):
+        cfg = Config(40000, sched, 13, prec, 1)
+        lazy = device_run(2, prob, cfg)
+        monkeypatch.setenv("PSA_LAZY", "0")
+        full = device_run(2, prob, cfg)
+        monkeypatch.delenv("PSA_LAZY")
+        assert not same_run(lazy, full), (sched, same_run(lazy, full))
