@@ -283,6 +283,9 @@ __global__ void __launch_bounds__(512) nm_kernel(const NMArgs a) {
     //  centroid prefixes before the first reordered position and (if the best
     //  vertex stays) every other diameter stay valid; w < 0: all are stale.
     auto exact_sort = [&](int w) {
+#ifdef PSA_NM_PROFILE
+        const long long xs0 = clock64();
+#endif
         if (tid == 0) ist[3] = n + 1;
         int has_nan = 0;
         for (int p = tid; p <= n; p += B) {
@@ -316,6 +319,9 @@ __global__ void __launch_bounds__(512) nm_kernel(const NMArgs a) {
         __syncthreads();
         if (keep_d) vertex_diameter(w, ord_s[0]);
         __syncthreads();
+#ifdef PSA_NM_PROFILE
+        if (rank == 0 && tid == 0) pc[5] += static_cast<unsigned long long>(clock64() - xs0);
+#endif
     };
     auto full_sort = [&]() {
         // a NaN value breaks the rank count below (it would share rank 0 with
@@ -517,8 +523,9 @@ __global__ void __launch_bounds__(512) nm_kernel(const NMArgs a) {
 #ifdef PSA_NM_PROFILE
     if (rank == 0 && tid == 0)
         printf("NMPROF iters=%d evals=%llu cyc_term=%llu cyc_centroid=%llu cyc_eval=%llu cyc_replace=%llu "
-               "cyc_shrink=%llu tie_sorts=%llu diam_full=%llu readd_len=%llu shrinks=%llu keep_d=%llu\n",
-               iter, evals, pf[0], pf[1], pf[2], pf[3], pf[4], pc[0], pc[1], pc[2], pc[3], pc[4]);
+               "cyc_shrink=%llu tie_sorts=%llu diam_full=%llu readd_len=%llu shrinks=%llu keep_d=%llu "
+               "cyc_exact_sort=%llu\n",
+               iter, evals, pf[0], pf[1], pf[2], pf[3], pf[4], pc[0], pc[1], pc[2], pc[3], pc[4], pc[5]);
 #endif
     const int b = ord_s[0];
     for (int j = tid; j < nc; j += B) a.x_best[c0 + j] = col(b, j);
