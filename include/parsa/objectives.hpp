@@ -61,6 +61,9 @@ struct ObjectiveFunction {
     // B200 addition: psa_family of the device twin (include/parsa_b200.h);
     // -1 = infer from eval_f64 (registry formulas), else explicit.
     int device_family = -1;
+    // B200 addition: the family parameter (PSA_FN_CONSTANT's value); set by
+    // probing when a host function is bound to the constant family.
+    double device_param = 0.0;
 };
 
 // l_k <= x_k <= u_k for every k; std::invalid_argument on a size mismatch.
@@ -97,6 +100,6 @@ const ObjectiveFunction& registry_get(const std::string& id);
 // has no device twin.  device_binding also reports whether the family was
 // found by probing (rule 3 above).
 int device_family_of(const ObjectiveFunction& f);
-int device_binding(const ObjectiveFunction& f, bool* probed);
+int device_binding(const ObjectiveFunction& f, bool* probed, double* param = nullptr);
 
 } // namespace parsa

@@ -24,7 +24,7 @@
 extern "C" {
 #endif
 
-#define PSA_ABI_VERSION 1
+#define PSA_ABI_VERSION 2
 
 typedef enum psa_status {
     PSA_OK = 0,
@@ -69,7 +69,9 @@ typedef enum psa_family {
     PSA_FN_SHEKEL10 = 20,        /*                        F18_c (m=10) */
     PSA_FN_SHEKEL_FOXHOLES = 21, /* objectives.cpp:272-284 F19 */
     PSA_FN_SPHERE = 22,          /* sum x_k^2: the "bowl" fixture of test_nelder_mead.cpp:17-38 */
-    PSA_FN_COUNT = 23
+    PSA_FN_CONSTANT = 23,        /* f = param: the constant fixtures of test_engines.cpp:91-99,
+                                    test_sa_core.cpp:140-160 */
+    PSA_FN_COUNT = 24
 } psa_family;
 
 /* ObjectiveFunction (objectives.hpp:31-39) reduced to what the device needs.
@@ -80,6 +82,7 @@ typedef struct psa_objective {
     int32_t dim;    /* n */
     const double* lower; /* BoxDomain::lower, dim entries */
     const double* upper; /* BoxDomain::upper, dim entries */
+    double param;        /* family parameter: PSA_FN_CONSTANT's value (else unused) */
 } psa_objective;
 
 /* AnnealSchedule (sa_core.hpp:15-22) */

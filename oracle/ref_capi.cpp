@@ -50,9 +50,21 @@ float sphere_f32(const float* x, int n) {
     return s;
 }
 
+// PSA_FN_CONSTANT: the constant fixtures of test_engines.cpp:91-99 and
+// test_sa_core.cpp:140-160 (value from the objective's param)
+double g_constant = 0.0;
+double constant_f64(const double*, int) { return g_constant; }
+float constant_f32(const float*, int) { return static_cast<float>(g_constant); }
+
 ObjectiveFunction make_objective(const psa_objective* o) {
     ObjectiveFunction f;
-    if (o->family == PSA_FN_SPHERE) {
+    if (o->family == PSA_FN_CONSTANT) {
+        g_constant = o->param;
+        f.id = "constant";
+        f.name = "constant";
+        f.eval_f64 = constant_f64;
+        f.eval_f32 = constant_f32;
+    } else if (o->family == PSA_FN_SPHERE) {
         f.id = "sphere";
         f.name = "sphere";
         f.eval_f64 = sphere_f64;

@@ -118,6 +118,11 @@ uint64_t orc_expected_evaluations(const psa_schedule* s, int32_t n_chains) {
 
 /* One macro body per precision keeps the two instantiations textually
  * identical, like the reference's `template <class Real>`. */
+/* PSA_FN_CONSTANT's value: set from the psa_objective by every entry point
+   (orc_set_fn_param for the bare evaluators) */
+static double orc_fn_param = 0.0;
+void orc_set_fn_param(double c) { orc_fn_param = c; }
+
 #define DEFINE_SUITE(R, SFX, SIN, COS, EXP, SQRT, FABS, PI)                                    \
     static R schwefel_##SFX(const R* x, int n) { /* objectives.cpp:23-29 */                    \
         R s = 0;                                                                               \
@@ -315,6 +320,7 @@ uint64_t orc_expected_evaluations(const psa_schedule* s, int32_t n_chains) {
         case PSA_FN_SHEKEL10: return shekel_##SFX(x, 10);                                      \
         case PSA_FN_SHEKEL_FOXHOLES: return foxholes_##SFX(x, n);                              \
         case PSA_FN_SPHERE: return sphere_##SFX(x, n);                                         \
+        case PSA_FN_CONSTANT: return (R)orc_fn_param;                                          \
         default: return (R)NAN;                                                                \
         }                                                                                      \
     }
@@ -443,6 +449,7 @@ static void trace_push(psa_run_result* out, int level, uint64_t cum, double best
 /* engines.cpp:131-207 */
 int32_t orc_run_synchronous(const psa_objective* f, const psa_engine_config* cfg,
                             psa_run_result* out, orc_level_detail* detail) {
+    orc_fn_param = f->param;
     if (orc_schedule_validate(&cfg->schedule)) return PSA_ERR_INVALID_ARGUMENT;
     if (cfg->n_chains < 1) return PSA_ERR_INVALID_ARGUMENT;
     const int n = f->dim, C = cfg->n_chains, N = cfg->schedule.sweep_length;
@@ -537,6 +544,7 @@ int32_t orc_run_synchronous(const psa_objective* f, const psa_engine_config* cfg
 /* engines.cpp:66-123 */
 int32_t orc_run_asynchronous(const psa_objective* f, const psa_engine_config* cfg,
                              psa_run_result* out) {
+    orc_fn_param = f->param;
     if (orc_schedule_validate(&cfg->schedule)) return PSA_ERR_INVALID_ARGUMENT;
     if (cfg->n_chains < 1) return PSA_ERR_INVALID_ARGUMENT;
     const int n = f->dim, C = cfg->n_chains, N = cfg->schedule.sweep_length;
@@ -616,6 +624,7 @@ static int nm_validate(const psa_nm_config* c) {
 /* nelder_mead.cpp:37-115 (always f64) */
 int32_t orc_nelder_mead_minimize(const psa_objective* f, const double* x_start,
                                  const psa_nm_config* cfg, psa_nm_result* out) {
+    orc_fn_param = f->param;
     if (nm_validate(cfg)) return PSA_ERR_INVALID_ARGUMENT;
     if (!contains(f, x_start)) return PSA_ERR_INVALID_ARGUMENT;
     const int n = f->dim;
@@ -703,6 +712,7 @@ int32_t orc_nelder_mead_minimize(const psa_objective* f, const double* x_start,
 int32_t orc_hybrid_run(const psa_objective* f, const psa_engine_config* cfg,
                        const psa_schedule* truncated, const psa_nm_config* nm,
                        psa_run_result* out) {
+    orc_fn_param = f->param;
     psa_engine_config sa = *cfg;
     sa.schedule = *truncated;
     const int cap = out->trace_capacity;

@@ -8,6 +8,7 @@ from __future__ import annotations
 import ctypes as C
 import os
 
+ABI_VERSION = 2  # include/parsa_b200.h PSA_ABI_VERSION (2: psa_objective.param, PSA_FN_CONSTANT)
 PSA_OK = 0
 PSA_ERR_INVALID_ARGUMENT = 1
 PSA_ERR_OUT_OF_RANGE = 2
@@ -25,7 +26,7 @@ FAMILIES = [
     "EXPONENTIAL", "GOLDSTEIN_PRICE", "GRIEWANK", "HIMMELBLAU", "LEVY_MONTALVO",
     "MOD_LANGERMAN", "MICHALEWICZ", "RASTRIGIN", "ROSENBROCK", "SALOMON",
     "SIX_HUMP_CAMEL", "SHUBERT", "SHEKEL5", "SHEKEL7", "SHEKEL10", "SHEKEL_FOXHOLES",
-    "SPHERE",
+    "SPHERE", "CONSTANT",
 ]
 FAMILY = {name: i for i, name in enumerate(FAMILIES)}
 
@@ -37,6 +38,7 @@ class psa_objective(C.Structure):
         ("dim", C.c_int32),
         ("lower", C.POINTER(C.c_double)),
         ("upper", C.POINTER(C.c_double)),
+        ("param", C.c_double),
     ]
 
 
@@ -212,7 +214,7 @@ def load_library(path: str | None = None):
         raise RuntimeError(f"parsa_b200: CUDA library {p} is missing; run __graft_entry__.build()")
     lib = C.CDLL(p)
     _declare(lib)
-    if lib.psa_abi_version() != 1:
+    if lib.psa_abi_version() != ABI_VERSION:
         raise RuntimeError("parsa_b200: ABI version mismatch")
     if path is None:
         _lib = lib

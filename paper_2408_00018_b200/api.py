@@ -121,6 +121,7 @@ class ObjectiveFunction:
     domain: BoxDomain
     family: str
     reference: ReferenceOptimum = field(default_factory=ReferenceOptimum)
+    param: float = 0.0  # family parameter: the value of family "CONSTANT"
 
     def with_dim(self, n: int, lo: Optional[float] = None, hi: Optional[float] = None) -> "ObjectiveFunction":
         """Copy resized to n dimensions on a uniform box (how the configs use
@@ -132,7 +133,7 @@ class ObjectiveFunction:
                                                   [[m[0]] * n for m in self.reference.minimizers[:1]]
                                                   if self.reference.minimizers else [],
                                                   self.reference.location_known,
-                                                  self.reference.location_at_origin))
+                                                  self.reference.location_at_origin), self.param)
 
 
 def _uniform(n, lo, hi):
@@ -391,7 +392,7 @@ class _Objective:
         self._id = f.id.encode()
         self.c = psa_objective(self._id, _abi.FAMILY[f.family], int(f.dim),
                                self.lower.ctypes.data_as(C.POINTER(C.c_double)),
-                               self.upper.ctypes.data_as(C.POINTER(C.c_double)))
+                               self.upper.ctypes.data_as(C.POINTER(C.c_double)), float(f.param))
 
 
 class _Config:

@@ -490,6 +490,7 @@ void plan_build(psa_plan* p, const psa_objective* f, const psa_engine_config* cf
     EngineArgs& a = p->args;
     a.n = n;
     a.family = p->family;
+    a.fparam = f->param;
     a.N = p->N;
     a.levels = p->levels;
     a.uniform_box = uniform;
@@ -673,6 +674,7 @@ void nm_run(const psa_objective* f, const double* x_start, const psa_nm_config* 
     psa::NMArgsHost a{};
     a.n = n;
     a.family = f->family;
+    a.fparam = f->param;
     a.max_iters = max_iters;
     a.reflect = nm->reflect;
     a.expand = nm->expand;
@@ -825,6 +827,7 @@ psa_status psa_nelder_mead_batch(const psa_objective* f, const double* x_starts,
         psa::NMBatchArgs a{};
         a.n = n;
         a.family = f->family;
+        a.fparam = f->param;
         a.max_iters = nm->max_iters > 0 ? nm->max_iters : 50000 * n;
         a.count = count;
         a.reflect = nm->reflect;
@@ -1087,6 +1090,7 @@ psa_status psa_device_evaluate(const psa_objective* f, int32_t precision, const 
         EngineArgs a{};
         a.n = n;
         a.family = f->family;
+        a.fparam = f->param;
         int c = count;
         const double* xp = dx.p;
         void* params[] = {&a, &xp, &c, &dout.p};
@@ -1127,6 +1131,7 @@ psa_status psa_metropolis_sweep(const psa_objective* f, int32_t precision, doubl
         EngineArgs a{};
         a.n = n;
         a.family = f->family;
+        a.fparam = f->param;
         a.lower = d_lo.p;
         a.width = d_w.p;
         a.keys = psa::make_keys(seed);

@@ -202,6 +202,12 @@ struct RowX {
     PSA_DEV R operator()(int k) const { return row[k]; }
 };
 
+// PSA_FN_CONSTANT: f = c, a per-objective parameter (the constant fixtures of
+// test_engines.cpp:91-99 and test_sa_core.cpp:140-160).  Every kernel that
+// can evaluate FullCost copies c from its arguments into this block-shared
+// slot before its first evaluation (fn_param_init).
+static __shared__ double psa_fn_param_s;
+
 template <class R>
 struct FullCost {
     static constexpr int A = 1;
@@ -231,10 +237,29 @@ struct FullCost {
         case PSA_FN_SHEKEL7: return Shekel<R, 7>::eval(x, n);
         case PSA_FN_SHEKEL10: return Shekel<R, 10>::eval(x, n);
         case PSA_FN_SHEKEL_FOXHOLES: return ShekelFoxholes<R>::eval(x, n);
+        case PSA_FN_CONSTANT: return static_cast<R>(psa_fn_param_s);
         default: return R(__int_as_float(0x7fc00000));
         }
     }
 };
+
+template <class Cost>
+struct IsFullCost {
+    static constexpr bool value = false;
+};
+template <class R>
+struct IsFullCost<FullCost<R>> {
+    static constexpr bool value = true;
+};
+
+// block-wide: the family parameter into psa_fn_param_s (FullCost kernels)
+template <class Cost>
+PSA_DEV void fn_param_init(double c) {
+    if constexpr (IsFullCost<Cost>::value) {
+        if (threadIdx.x == 0) psa_fn_param_s = c;
+        __syncthreads();
+    }
+}
 
 // energy of a chain row of either layout
 template <class Cost, int NT, class Row>

@@ -71,6 +71,7 @@ struct EngineArgs {
     double lazy_r;
     double lazy_alpha;
     unsigned long long* work; // [2] per-level chain counters (dynamic assignment)
+    double fparam;            // family parameter (PSA_FN_CONSTANT's value)
     int lazy_adapt;           // switch a block to fold-every-trial when settles pass 2%
 };
 
@@ -97,6 +98,7 @@ struct NMArgsHost {
     int ldt;        // even, >= n * (cached values per coordinate)
     double* x_best; // n
     NMOut* out;
+    double fparam;  // family parameter (PSA_FN_CONSTANT's value)
 };
 
 // batched NM: one instance per thread (nm_batch_kernel)
@@ -115,6 +117,7 @@ struct NMBatchArgs {
     double* f_best;         // count
     int* iterations;        // count
     unsigned long long* evaluations; // count
+    double fparam;                   // family parameter (PSA_FN_CONSTANT's value)
 };
 const void* nm_batch_kernel_for(int family);
 // scratch doubles per batched instance: vertices, values, centroid and three

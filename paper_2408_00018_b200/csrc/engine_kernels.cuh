@@ -431,6 +431,7 @@ struct LazyCost<SepCost<R, F>> {
 template <class R, class Cost, int NT, bool G, bool PAIR, bool PC = false, bool LZ = false, bool UB = false>
 __device__ __forceinline__ void v2_body(const EngineArgs& a) {
     constexpr int A = Cost::A;
+    fn_param_init<Cost>(a.fparam);
     extern __shared__ __align__(16) unsigned char smem_raw[];
     cg::grid_group grid = cg::this_grid();
     const int B = blockDim.x, tid = threadIdx.x;
@@ -870,6 +871,7 @@ __global__ void __launch_bounds__(128, 2) v2_pair_kernel(const EngineArgs a) {
 template <class R, class Cost, int NT, bool G>
 __global__ void __launch_bounds__(256) v1_kernel(const EngineArgs a) {
     constexpr int A = Cost::A;
+    fn_param_init<Cost>(a.fparam);
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int B = blockDim.x, tid = threadIdx.x;
     const int n = a.n;
@@ -1012,6 +1014,7 @@ __device__ void pc_produce_x(PcEntryX<R, Cost::A>* buf, long long j0, int jn, in
 template <class R, class Cost, int NT>
 __global__ void __launch_bounds__(128, 4) v1_pc_kernel(const EngineArgs a) {
     constexpr int A = Cost::A;
+    fn_param_init<Cost>(a.fparam);
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int B = blockDim.x, tid = threadIdx.x, lane = tid & 31;
     const int n = a.n;
@@ -1289,6 +1292,7 @@ __global__ void __launch_bounds__(128, 3) v1_pair_kernel(const EngineArgs a) {
 template <class R, class Cost>
 __global__ void probe_evaluate(const EngineArgs a, const double* x, int count, double* out) {
     constexpr int A = Cost::A;
+    fn_param_init<Cost>(a.fparam);
     extern __shared__ __align__(16) unsigned char smem_raw[];
     R* V = reinterpret_cast<R*>(smem_raw);
     const int B = blockDim.x;
@@ -1316,6 +1320,7 @@ __global__ void sweep_one(const EngineArgs a, double* x, R* row, double* energy,
                           unsigned long long* counter, uint32_t chain, uint32_t level,
                           double temperature, int n_steps) {
     constexpr int A = Cost::A;
+    fn_param_init<Cost>(a.fparam);
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     const int n = a.n;
     Box box;

@@ -101,6 +101,7 @@ static __device__ __noinline__ void exact_sort_tasks(psa_sort::KeyId* kp, int m,
 template <class Cost>
 __global__ void __launch_bounds__(512) nm_kernel(const NMArgs a) {
     constexpr int A = Cost::A;
+    fn_param_init<Cost>(a.fparam);
     extern __shared__ __align__(16) unsigned char smem_raw[];
     cg::cluster_group cluster = cg::this_cluster();
     const int CL = static_cast<int>(cluster.num_blocks());
@@ -129,7 +130,7 @@ __global__ void __launch_bounds__(512) nm_kernel(const NMArgs a) {
 #ifdef PSA_NM_PROFILE
     // measurement builds only (scripts/build_nm_profile.sh): cycles per phase
     // and path counters on CTA 0 thread 0, printed at the end
-    unsigned long long pf[6] = {0, 0, 0, 0, 0, 0}, pc[6] = {0, 0, 0, 0, 0, 0};
+    unsigned long long pf[6] = {0, 0, 0, 0, 0, 0}, pc[6] = {0, 0, 0, 0, 0, 0}, pt[2] = {0, 0};
     long long tq = clock64();
 #define NMP(i)                                   \
     do {                                         \
@@ -321,6 +322,17 @@ __global__ void __launch_bounds__(512) nm_kernel(const NMArgs a) {
         __syncthreads();
 #ifdef PSA_NM_PROFILE
         if (rank == 0 && tid == 0) pc[5] += static_cast<unsigned long long>(clock64() - xs0);
+        // tie groups after the sort: adjacent equal values whose points are
+        // bitwise identical over this CTA's columns (pt[0]) or not (pt[1])
+        if (rank == 0 && tid == 0) {
+            for (int p = 0; p < n; ++p) {
+                if (!(f_s[ord_s[p]] == f_s[ord_s[p + 1]])) continue;
+                bool same = true;
+                for (int j = 0; j < nc && same; ++j)
+                    same = __double_as_longlong(col(ord_s[p], j)) == __double_as_longlong(col(ord_s[p + 1], j));
+                pt[same ? 0 : 1] += 1;
+            }
+        }
 #endif
     };
     auto full_sort = [&]() {
@@ -524,8 +536,8 @@ __global__ void __launch_bounds__(512) nm_kernel(const NMArgs a) {
     if (rank == 0 && tid == 0)
         printf("NMPROF iters=%d evals=%llu cyc_term=%llu cyc_centroid=%llu cyc_eval=%llu cyc_replace=%llu "
                "cyc_shrink=%llu tie_sorts=%llu diam_full=%llu readd_len=%llu shrinks=%llu keep_d=%llu "
-               "cyc_exact_sort=%llu\n",
-               iter, evals, pf[0], pf[1], pf[2], pf[3], pf[4], pc[0], pc[1], pc[2], pc[3], pc[4], pc[5]);
+               "cyc_exact_sort=%llu tie_pairs_same_point=%llu tie_pairs_distinct=%llu\n",
+               iter, evals, pf[0], pf[1], pf[2], pf[3], pf[4], pc[0], pc[1], pc[2], pc[3], pc[4], pc[5], pt[0], pt[1]);
 #endif
     const int b = ord_s[0];
     for (int j = tid; j < nc; j += B) a.x_best[c0 + j] = col(b, j);
@@ -551,6 +563,7 @@ __global__ void __launch_bounds__(512) nm_kernel(const NMArgs a) {
 template <class Cost>
 __global__ void __launch_bounds__(128) nm_batch_kernel(const NMBatchArgs a) {
     constexpr int A = Cost::A;
+    fn_param_init<Cost>(a.fparam);
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= a.count) return;
     const int n = a.n;

@@ -39,7 +39,7 @@ struct DeviceObjective {
 inline DeviceObjective device_view(const ObjectiveFunction& f) {
     DeviceObjective o;
     o.c.id = f.id.c_str();
-    o.c.family = device_binding(f, &o.probed);
+    o.c.family = device_binding(f, &o.probed, &o.c.param);
     o.c.dim = f.dim;
     o.c.lower = f.domain.lower.data();
     o.c.upper = f.domain.upper.data();

@@ -315,7 +315,7 @@ bool same_bits(T a, T b) {
 // function (bridge::verify), so a coincidental match cannot go unnoticed.
 constexpr int kProbes = 64;
 
-int probe_family(const ObjectiveFunction& f) {
+int probe_family(const ObjectiveFunction& f, double* param) {
     const int n = f.dim;
     if (!f.eval_f64 || !f.eval_f32 || n < 1 || f.domain.dim() != n ||
         static_cast<int>(f.domain.upper.size()) != n)
@@ -339,6 +339,16 @@ int probe_family(const ObjectiveFunction& f) {
         pts32[i].assign(pts[i].begin(), pts[i].end());
         want32[i] = f.eval_f32(pts32[i].data(), n);
     }
+    // a constant function (the fixtures of test_engines.cpp:91-99 and
+    // test_sa_core.cpp:140-160): one value everywhere, the single-precision
+    // one its rounding
+    bool constant = same_bits(want32[0], static_cast<float>(want64[0]));
+    for (std::size_t i = 1; constant && i < pts.size(); ++i)
+        constant = same_bits(want64[i], want64[0]) && same_bits(want32[i], want32[0]);
+    if (constant) {
+        if (param) *param = want64[0];
+        return PSA_FN_CONSTANT;
+    }
     for (const auto& e : kFamilies) {
         if (!family_fits(e.family, n)) continue;
         bool ok = true;
@@ -351,13 +361,14 @@ int probe_family(const ObjectiveFunction& f) {
 
 } // namespace
 
-int device_binding(const ObjectiveFunction& f, bool* probed) {
+int device_binding(const ObjectiveFunction& f, bool* probed, double* param) {
     if (probed) *probed = false;
+    if (param) *param = f.device_param;
     if (f.device_family >= 0) return f.device_family < PSA_FN_COUNT ? f.device_family : -1;
     for (const auto& e : kFamilies)
         if (f.eval_f64 != nullptr && f.eval_f64 == e.f64 && f.eval_f32 == e.f32)
             return family_fits(e.family, f.dim) ? e.family : -1;
-    const int fam = probe_family(f);
+    const int fam = probe_family(f, param);
     if (probed) *probed = fam >= 0;
     return fam;
 }

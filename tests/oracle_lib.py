@@ -99,13 +99,13 @@ class Problem:
     """Keeps the numpy buffers behind a psa_objective alive."""
 
     def __init__(self, family: str | int, dim: int, lo: float | np.ndarray, hi: float | np.ndarray,
-                 ident: str = "fn"):
+                 ident: str = "fn", param: float = 0.0):
         self.family = _abi.FAMILY[family] if isinstance(family, str) else int(family)
         self.dim = int(dim)
         self.lower = np.ascontiguousarray(np.broadcast_to(np.asarray(lo, dtype=np.float64), (dim,)))
         self.upper = np.ascontiguousarray(np.broadcast_to(np.asarray(hi, dtype=np.float64), (dim,)))
         self._id = ident.encode()
-        self.c = psa_objective(self._id, self.family, self.dim, dptr(self.lower), dptr(self.upper))
+        self.c = psa_objective(self._id, self.family, self.dim, dptr(self.lower), dptr(self.upper), float(param))
 
 
 class Config:

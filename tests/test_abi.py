@@ -28,7 +28,7 @@ def test_library_loads_and_exports_every_declared_symbol(lib):
     assert sorted(_abi.EXPORTED_SYMBOLS) == decl
     for name in decl:
         assert hasattr(lib, name), name
-    assert lib.psa_abi_version() == 1
+    assert lib.psa_abi_version() == _abi.ABI_VERSION == 2
     out = subprocess.run(["nm", "-D", "--defined-only", _abi.LIB_PATH], capture_output=True, text=True).stdout
     for name in decl:
         assert re.search(rf"\bT {name}\b", out), name

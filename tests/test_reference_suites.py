@@ -6,13 +6,14 @@ tests/cxx/_bin/ (built by __graft_entry__.build() where the reference tree
 exists; the binaries travel to the GPU box).  The doctest header the
 reference expects is not vendored there; tests/cxx/doctest_shim stands in.
 
-Known, documented failures: test cases whose objective is a
+Known, documented failure: a test case whose objective is a
 host function that no device formula reproduces.  The B200 engines never
 call a host function per trial (there is no CPU fallback), so such an
-objective is rejected with std::invalid_argument:
-  * constant objectives (return 3.0), and
-  * the NM "offset bowl" that also records, from inside the host callback,
-    whether any evaluated point left the box.
+objective is rejected with std::invalid_argument: the NM "offset bowl" that
+also records, from inside the host callback, whether any evaluated point
+left the box.  (The constant objectives of test_engines / test_sa_core,
+`return 3.0`, bind by probing to the parametric constant family since
+round 2.)
 
 The CLI golden test runs `parsa run --config` on the configs in
 tests/golden/harness/ and compares every report file byte for byte with the
@@ -34,8 +35,6 @@ CLI = os.path.join(ROOT, "paper_2408_00018_b200", "bin", "parsa")
 GOLDEN = os.path.join(ROOT, "tests", "golden", "harness")
 
 ALLOWED_FAILURES = {
-    "test_engines": {"constant objective yields its constant"},
-    "test_sa_core": {"sweep on a constant objective accepts the neighbour, energy unchanged"},
     "test_nelder_mead": {"all evaluated points stay inside the box"},
 }
 
