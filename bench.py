@@ -160,6 +160,27 @@ def reference_sample(precision: int, seconds: float):
     return rate, sample, threads, chains, res.c.evaluations, wall
 
 
+def reference_v0_ms(precision: int):
+    """parsa_ref::run_sequential (one chain, one host thread — the reference
+    engine's own latency path) on the V0 entry's workload: ms per run."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle_lib import Config, Problem, Result, ref
+
+    lib = ref()
+    if lib is None:
+        return None
+    prob = Problem("SCHWEFEL", 10, -512.0, 512.0, ident="F0_a")
+    cfg = Config(1, SCHEDULE, 0, precision, 0, workers=1)
+    res = Result(10, 1200)
+    best = None
+    for _ in range(3):
+        rc = lib.ref_run(0, C.byref(prob.c), C.byref(cfg.c), C.byref(res.c))
+        if rc != 0:
+            return None
+        best = res.c.wall_time_s if best is None else min(best, res.c.wall_time_s)
+    return best * 1e3
+
+
 def run_reference_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -292,6 +313,14 @@ def measure_configs(psa, torch, flush):
     for prec in (psa.Precision.f32, psa.Precision.f64):
         entry("C1", "configs[0]: synchronous SA, Schwefel n=10, 1024 chains, paper ladder", "F0_a",
               schw.with_dim(10), psa.EngineConfig(n_chains=1024, schedule=paper, precision=prec), 2, 3)
+    # V0 (run_sequential = V1 with one chain, engines.cpp:125-129): a latency
+    # path — one chain through the whole ladder (114600 dependent trials)
+    entry("V0", "run_sequential: one chain, Schwefel n=10, paper ladder (latency)", "F0_a", schw.with_dim(10),
+          psa.EngineConfig(n_chains=1, schedule=paper, precision=psa.Precision.f32), 1, 3)
+    try:
+        out[-1]["reference_ms"] = reference_v0_ms(1)  # the reference's own V0 on one host core
+    except Exception:  # pragma: no cover - reported as missing
+        out[-1]["reference_ms"] = None
     for fid in ("F0_a", "F1_a", "F13_a"):
         f = psa.registry_get(fid)
         f = f if f.dim == 30 else f.with_dim(30)

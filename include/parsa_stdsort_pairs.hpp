@@ -228,4 +228,206 @@ inline void sort_tasks(KeyId* v, int m) {
 }
 #endif
 
+#if defined(__CUDACC__)
+// ---------------------------------------------------------------------------
+// The same sort, warp-cooperative (device): sort() on (key, id) pairs with
+// the whole warp instead of one lane per range — the order of sort()
+// exactly, in any task order (see range_task above):
+//  * a split's unguarded_partition is emulated with ballots.  With Ls the
+//    ascending left-stop positions (!(v[i] < P)) and Rs the descending
+//    right-stop positions (!(P < v[j])) of the ORIGINAL range, the two-pointer
+//    scan swaps (Ls[k], Rs[k]) for every k < K, K the first k with
+//    !(Ls[k] < Rs[k]) (both lists are monotone, and every swap touches only
+//    positions both scans have already passed), and returns
+//    K == 0 ? Ls[0] : min(Ls[K], Rs[K-1]) (position Rs[K-1] then holds a
+//    left-stop value);
+//  * heap_sort's make_heap runs the sift-downs of one tree depth in
+//    parallel (their subtrees are disjoint, and the sequential loop visits
+//    every deeper node first); its sort_heap phase stays on one lane;
+//  * final insertion sorts run one range per lane.
+// All 32 lanes call warp_sort; v, ls, rs (m ints each) and the range lists
+// (WarpSortLists) are in shared memory.
+// ---------------------------------------------------------------------------
+struct WarpSortLists {
+    int* cur;   // 3 ints per range: first, last, depth
+    int* nxt;
+    int* small; // 2 ints per final range (<= PSA_SORT_THRESHOLD elements)
+};
+
+__device__ inline int warp_partition(KeyId* v, int first, int last, int* ls, int* rs) {
+    const int lane = threadIdx.x & 31;
+    const unsigned below = (1u << lane) - 1u;
+    const double P = v[first].key;
+    int nl = 0, nr = 0;
+    for (int base = first + 1; base < last; base += 32) {
+        const int i = base + lane;
+        const bool in = i < last;
+        const double k = in ? v[i].key : 0.0;
+        const bool L = in && !(k < P);
+        const bool R = in && !(P < k);
+        const unsigned bl = __ballot_sync(0xffffffffu, L), br = __ballot_sync(0xffffffffu, R);
+        if (L) ls[nl + __popc(bl & below)] = i;
+        if (R) rs[nr + __popc(br & below)] = i; // ascending; Rs[k] = rs[nr - 1 - k]
+        nl += __popc(bl);
+        nr += __popc(br);
+    }
+    __syncwarp();
+    const int mk = nl < nr ? nl : nr;
+    int K = mk;
+    for (int base = 0; base < mk; base += 32) {
+        const int k = base + lane;
+        const unsigned bf = __ballot_sync(0xffffffffu, k < mk && !(ls[k] < rs[nr - 1 - k]));
+        if (bf) {
+            K = base + __ffs(bf) - 1;
+            break;
+        }
+    }
+    for (int k = lane; k < K; k += 32) swap(v, ls[k], rs[nr - 1 - k]);
+    __syncwarp();
+    if (K == 0) return ls[0];
+    const int r = rs[nr - K];
+    return K < nl && ls[K] < r ? ls[K] : r;
+}
+
+// adjust_heap by the whole warp: the hole's descent follows, level by level,
+// the child chosen by `second = right; if (v[right] < v[left]) second--` —
+// a path that depends only on the heap, not on the value sifted.  The warp
+// loads the 30 descendants of the current node four levels deep at once
+// (lane j: depth L = floor(log2(j + 2)), offset o = j + 2 - 2^L, node
+// (s + 1) 2^L - 1 + o), every odd lane (a right child) decides its pair,
+// and the path through the four levels is read off one ballot; the chosen
+// nodes move up into their parents' places in parallel (all loads precede
+// all stores).  The descent stops where the sequential loop would
+// (second >= (len - 1) / 2); the tail (a lone left child) and push_heap
+// run on lane 0.  Same moves, same order of effect, as adjust_heap.
+__device__ inline void warp_adjust_heap(KeyId* v, int first, int hole, int len, KeyId value) {
+    const int lane = threadIdx.x & 31;
+    KeyId* b = v + first;
+    const int top = hole;
+    const int lim = (len - 1) / 2;
+    int second = hole;
+    const int L = lane < 30 ? 31 - __clz(lane + 2) : 0;
+    const int o = lane + 2 - (1 << L);
+    while (second < lim) {
+        const int node = ((second + 1) << L) - 1 + o;
+        KeyId mine{0.0, 0, 0};
+        if (lane < 30 && node < len) mine = b[node];
+        const double sib = __shfl_up_sync(0xffffffffu, mine.key, 1);
+        // odd o: a right child; it wins its pair unless it is less than the left
+        const unsigned rw = __ballot_sync(0xffffffffu, lane < 30 && (o & 1) && !(mine.key < sib));
+        // walk the (up to) four levels
+        int path[4];
+        int depth = 0, oo = 0, s = second;
+#pragma unroll
+        for (int k = 1; k <= 4; ++k) {
+            if (s >= lim) break;
+            const int right_lane = (1 << k) - 2 + 2 * oo + 1; // lane of the right child at depth k
+            oo = 2 * oo + static_cast<int>((rw >> right_lane) & 1u);
+            path[k - 1] = (1 << k) - 2 + oo; // lane of the chosen node
+            s = ((second + 1) << k) - 1 + oo;
+            depth = k;
+        }
+        // moves: chosen node at depth k goes to its parent's place (the hole
+        // for k = 1); lanes holding chosen nodes store in parallel
+#pragma unroll
+        for (int k = 1; k <= 4; ++k) {
+            if (k <= depth && lane == path[k - 1]) {
+                const int parent = k == 1 ? hole : ((second + 1) << (k - 1)) - 1 + (o >> 1);
+                b[parent] = mine;
+            }
+        }
+        hole = s;
+        second = s;
+        __syncwarp();
+    }
+    if (lane == 0) {
+        if ((len & 1) == 0 && second == (len - 2) / 2) {
+            second = 2 * (second + 1);
+            b[hole] = b[second - 1];
+            hole = second - 1;
+        }
+        push_heap(v, first, hole, top, value);
+    }
+    __syncwarp();
+}
+
+__device__ inline void warp_heap_sort(KeyId* v, int first, int last) {
+    const int lane = threadIdx.x & 31;
+    const int len = last - first;
+    if (len >= 2) {
+        const int lastp = (len - 2) / 2;
+        for (int d = 31 - __clz(lastp + 1); d >= 0; --d) { // deepest parents first
+            const int lo = (1 << d) - 1, hi = min((1 << (d + 1)) - 2, lastp);
+            for (int p = lo + lane; p <= hi; p += 32) {
+                const KeyId value = v[first + p];
+                adjust_heap(v, first, p, len, value);
+            }
+            __syncwarp();
+        }
+    }
+    while (last - first > 1) {
+        --last;
+        const KeyId value = v[last];
+        __syncwarp();
+        if (lane == 0) v[last] = v[first];
+        __syncwarp();
+        warp_adjust_heap(v, first, 0, last - first, value);
+    }
+}
+
+__device__ inline void warp_sort(KeyId* v, int m, int* ls, int* rs, WarpSortLists L) {
+    const int lane = threadIdx.x & 31;
+    if (m <= PSA_SORT_THRESHOLD) {
+        if (lane == 0) insertion_sort(v, 0, m);
+        __syncwarp();
+        return;
+    }
+    int* cur = L.cur;
+    int* nxt = L.nxt;
+    if (lane == 0) {
+        cur[0] = 0;
+        cur[1] = m;
+        cur[2] = psa_lg(m) * 2;
+    }
+    __syncwarp();
+    int nc = 1;
+    while (nc > 0) {
+        int nn = 0, ns = 0; // warp-uniform
+        for (int r = 0; r < nc; ++r) {
+            const int f = cur[3 * r], l = cur[3 * r + 1], d = cur[3 * r + 2];
+            if (d == 0) {
+                warp_heap_sort(v, f, l);
+                continue;
+            }
+            if (lane == 0) median_to_first(v, f, f + 1, f + (l - f) / 2, l - 1);
+            __syncwarp();
+            const int cut = warp_partition(v, f, l, ls, rs);
+            if (lane == 0) {
+                if (cut - f > PSA_SORT_THRESHOLD) {
+                    nxt[3 * nn] = f; nxt[3 * nn + 1] = cut; nxt[3 * nn + 2] = d - 1;
+                } else {
+                    L.small[2 * ns] = f; L.small[2 * ns + 1] = cut;
+                }
+                if (l - cut > PSA_SORT_THRESHOLD) {
+                    const int q = nn + (cut - f > PSA_SORT_THRESHOLD);
+                    nxt[3 * q] = cut; nxt[3 * q + 1] = l; nxt[3 * q + 2] = d - 1;
+                } else {
+                    const int q = ns + (cut - f <= PSA_SORT_THRESHOLD);
+                    L.small[2 * q] = cut; L.small[2 * q + 1] = l;
+                }
+            }
+            nn += (cut - f > PSA_SORT_THRESHOLD) + (l - cut > PSA_SORT_THRESHOLD);
+            ns += (cut - f <= PSA_SORT_THRESHOLD) + (l - cut <= PSA_SORT_THRESHOLD);
+            __syncwarp();
+        }
+        for (int i = lane; i < ns; i += 32) insertion_sort(v, L.small[2 * i], L.small[2 * i + 1]);
+        __syncwarp();
+        int* t = cur;
+        cur = nxt;
+        nxt = t;
+        nc = nn;
+    }
+}
+#endif
+
 } // namespace psa_sort

@@ -256,6 +256,7 @@ struct psa_plan {
     bool pair = false;            // two chains per thread (v2_pair_kernel)
     bool pc = false;              // producer/consumer blocks (v2_pc_kernel)
     bool lazy = false;            // deferred fold (v2_lazy_kernel)
+    bool lazy_pc = false;         // producer/consumer with the deferred-fold consumer
     uint64_t last_settles = 0;    // exact-fold decisions of the last fetched run
     size_t mask_stride = 0;
     const void* kernel = nullptr; // the engine kernel this plan launches
@@ -337,7 +338,8 @@ void plan_build(psa_plan* p, const psa_objective* f, const psa_engine_config* cf
     // producer/consumer kernel's overlap wins (measured: C1, C3), so the
     // deferred fold is the default only at larger chain counts.
     const bool few_chains = static_cast<long long>(p->chains_local) < 256ll * lim.sms;
-    p->lazy = engine == 2 && p->ks.v2z && !(lazy_env && lazy_env[0] == '0') &&
+    const bool lazy_allowed = p->ks.v2z && !(lazy_env && lazy_env[0] == '0');
+    p->lazy = engine == 2 && lazy_allowed &&
               ((mode.empty() && !few_chains) || mode == "lazy" || mode == "lazy1" || mode == "lazypair");
     // block size: of 128/96/64/32 threads, the one that keeps the most
     // chain rows resident per SM (large rows: three 32-thread blocks hold
@@ -379,7 +381,7 @@ void plan_build(psa_plan* p, const psa_objective* f, const psa_engine_config* cf
     // when the ladder stays above rr * n (measured: settles <= 0.2% at
     // n = 500 down to T ~ rr n / 1); binary64 intervals are ~1e-12 wide.
     double lazy_rr = 0;
-    if (p->lazy) {
+    if (lazy_allowed) {
         std::vector<double> upper(n);
         for (int k = 0; k < n; ++k) upper[k] = f->lower[k] + width[k];
         lazy_rr = p->ks.lazy_radius(n, f->lower, upper.data());
@@ -404,10 +406,15 @@ void plan_build(psa_plan* p, const psa_objective* f, const psa_engine_config* cf
     const bool heavy_finish = p->family == PSA_FN_ACKLEY || p->family == PSA_FN_EXPONENTIAL ||
                               p->family == PSA_FN_SALOMON;
     const bool few = static_cast<long long>(p->chains_local) < 256ll * lim.sms && !heavy_finish;
-    const void* pc_kern = engine == 2 ? p->ks.v2pc : p->ks.v1pc;
+    // (affine families: the consumer warp uses the deferred fold, v2_lazy_pc_kernel)
+    const bool lazy_pc = lazy_allowed && (engine == 2 ? p->ks.v2pcz : p->ks.v1pcz) &&
+                         (mode.empty() || mode == "lazypc");
+    const void* pc_kern = engine == 2 ? (lazy_pc ? p->ks.v2pcz : p->ks.v2pc) : (lazy_pc ? p->ks.v1pcz : p->ks.v1pc);
     const size_t smem_pc = engine == 2 ? p->ks.smem_v2pc(n, 128, !uniform) : p->ks.smem_v1pc(n, 128, !uniform);
-    if (!p->lazy && !p->hbm_rows && pc_kern && (mode == "pc" || (mode.empty() && few)) && smem_pc <= smem_cap) {
+    if (!p->lazy && !p->hbm_rows && pc_kern && (mode == "pc" || mode == "lazypc" || (mode.empty() && few)) &&
+        smem_pc <= smem_cap) {
         p->pc = true;
+        p->lazy_pc = lazy_pc;
         p->block = B = 128;
         p->smem = smem_pc;
         kern = pc_kern;
@@ -527,7 +534,7 @@ void plan_build(psa_plan* p, const psa_objective* f, const psa_engine_config* cf
     a.world = p->world;
     a.rank = p->rank;
     a.spin_limit = 60ll * 2000000000ll; // ~60 s at 2 GHz
-    if (p->lazy) {
+    if (p->lazy || p->lazy_pc) {
         a.lazy_r = lazy_rr;
         const char* adapt = std::getenv("PSA_LAZY_ADAPT"); // 0: never fall back (tests)
         a.lazy_adapt = !(adapt && adapt[0] == '0');
@@ -998,12 +1005,14 @@ psa_status psa_plan_describe(const psa_plan* p, char* buf, int32_t capacity) {
     return guarded([&] {
         if (!p || !buf || capacity < 1) fail(PSA_ERR_INVALID_ARGUMENT, "parsa_b200: null argument");
         std::ostringstream d;
-        const char* layout = p->engine == 1 ? (p->pc         ? "v1_pc_kernel (producer/consumer warps, 32 chains per block)"
+        const char* layout = p->engine == 1 ? (p->pc && p->lazy_pc ? "v1_lazy_pc_kernel (deferred-fold consumer, producer/consumer warps, 32 chains per block)"
+                                               : p->pc         ? "v1_pc_kernel (producer/consumer warps, 32 chains per block)"
                                                : p->pair       ? "v1_pair_kernel (two chains per thread, shared-memory pair rows)"
                                                : p->hbm_rows ? "v1_kernel (HBM SoA rows)"
                                                              : "v1_kernel (shared-memory rows)")
                              : p->lazy && p->pair ? "v2_lazy_pair_kernel (deferred fold, two chains per thread, shared-memory pair rows)"
                              : p->pair     ? "v2_pair_kernel (two chains per thread, shared-memory pair rows)"
+                             : p->pc && p->lazy_pc ? "v2_lazy_pc_kernel (deferred-fold consumer, producer/consumer warps, 32 chains per block)"
                              : p->pc       ? "v2_pc_kernel (producer/consumer warps, 32 chains per block)"
                              : p->lazy     ? (p->hbm_rows ? "v2_lazy_kernel (deferred fold, HBM SoA rows)"
                                                               : "v2_lazy_kernel (deferred fold, one chain per thread, shared-memory rows)")

@@ -152,6 +152,8 @@ struct EngineKernels {
     const void* v2gz; // HBM rows
     const void* v2gzu; // HBM rows, uniform box
     const void* v2pz; // chain pairs (binary32), shared-memory pair rows
+    const void* v2pcz; // producer/consumer blocks with the deferred-fold consumer
+    const void* v1pcz; // V1 producer/consumer blocks with the deferred-fold consumer
     double (*lazy_radius)(int n, const double* lower, const double* upper);
     double (*lazy_alpha_of)(int n);
 };

@@ -250,6 +250,94 @@ __device__ R pc_sweep(R* row, int n_rt, int family, R E, double temperature, uin
     return E;
 }
 
+// The consumer of pc_sweep with the deferred fold (engine.cuh, sweep_lazy):
+// the ring entry's new term and the replaced term give the interval of the
+// energy difference, and the consumer folds only to settle a straddling
+// decision and once at the end of the level.  Producers are unchanged.
+template <class R, class Cost, int NT>
+__device__ R pc_sweep_lazy(R* row, int n_rt, int family, R E, double temperature, uint32_t chain_base,
+                           uint32_t level, uint32_t ctr0, int N, const Box& box, const PhiloxKeys& keys,
+                           uint32_t* mask, size_t mask_stride, bool live, PcEntry<R, Cost::A>* buf, int& slot,
+                           bool prefilled, bool prefetch_next, R rr, R alpha, SweepStats& st) {
+    using L = LazyOf<typename Cost::Fam>;
+    static_assert(Cost::A == 1, "deferred fold: one accumulator");
+    const int n = NT > 0 ? NT : n_rt;
+    const float k2 = metropolis_k2(temperature);
+    const bool producer = threadIdx.x >= 32;
+    const int lane = threadIdx.x & 31;
+    const int rounds = (N + 31) / 32;
+    const R sa = L::sigma > 0 ? alpha : -alpha;
+    bool have = true;
+    auto at = [&](int k) { return buf + ((slot + k) % 3) * 1024; };
+    if (!prefilled) {
+        if (producer) pc_produce<R, Cost>(at(0), 0, N < 32 ? N : 32, n, chain_base, level, ctr0, box, keys);
+        __syncthreads();
+    }
+    const bool short_last = rounds > 1 && N - 32 * (rounds - 1) <= 16;
+    for (int k = 0; k < rounds; ++k) {
+        const int jn = N - 32 * k < 32 ? N - 32 * k : 32;
+        if (producer) {
+            if (k + 1 < rounds) {
+                const int j1 = 32 * (k + 1);
+                pc_produce<R, Cost>(at(k + 1), j1, N - j1 < 32 ? N - j1 : 32, n, chain_base, level, ctr0, box, keys);
+            }
+            const bool early = short_last && k + 2 == rounds, late = !short_last && k + 1 == rounds;
+            if (prefetch_next && (early || late))
+                pc_produce<R, Cost>(at(rounds), 0, N < 32 ? N : 32, n, chain_base, level + 1, 0u, box, keys);
+        } else if (live) {
+            const PcEntry<R, 1>* cur = at(k);
+            uint32_t word = 0;
+            PcEntry<R, 1> nx = cur[lane];
+            for (int j = 0; j < jn; ++j) {
+                const PcEntry<R, 1> en = nx;
+                nx = cur[(j + 1 < jn ? j + 1 : j) * 32 + lane];
+                const R to = row[en.d];
+                const MBand b = metropolis_band(en.m);
+                const R q = (en.t[0] - to) * sa;
+                const R hi = q + rr, lo = q - rr;
+                int r = ((hi <= R(0)) | (static_cast<float>(hi) * k2 < b.lo))
+                            ? 1
+                            : (((lo > R(0)) & (static_cast<float>(lo) * k2 > b.hi)) ? 0 : -1);
+                bool settled = false;
+                if (__any_sync(__activemask(), r < 0)) {
+                    if (__any_sync(__activemask(), (r < 0) & !have)) {
+                        const R eo = Cost::template energy<NT>(row, n, family);
+                        if (!have) {
+                            E = eo;
+                            have = true;
+                        }
+                    }
+                    if (r < 0) row[en.d] = en.t[0];
+                    const R et = Cost::template energy<NT>(row, n, family);
+                    if (r < 0) {
+                        int v = metropolis_fast<R>(et, E, k2, b);
+                        if (v < 0)
+                            v = Accept<R>::exact(static_cast<double>(et) - static_cast<double>(E), temperature, en.m);
+                        if (v) E = et;
+                        else row[en.d] = to;
+                        r = v;
+                        settled = true;
+                        st.settles += 1;
+                    }
+                }
+                if (r && !settled) {
+                    row[en.d] = en.t[0];
+                    have = false;
+                }
+                word |= static_cast<uint32_t>(r) << j;
+            }
+            mask[static_cast<size_t>(k) * mask_stride] = word;
+        }
+        __syncthreads();
+    }
+    if (!producer && live && __any_sync(__activemask(), !have)) {
+        const R e = Cost::template energy<NT>(row, n, family);
+        if (!have) E = e;
+    }
+    slot = (slot + rounds) % 3;
+    return E;
+}
+
 // draw_random_start (engines.cpp:43-46): coordinate k uses draw k of (seed, c, 0)
 __device__ __forceinline__ double random_start_coord(const EngineArgs& a, const Box& box,
                                                      uint32_t c, int k) {
@@ -513,10 +601,17 @@ __device__ __forceinline__ void v2_body(const EngineArgs& a) {
                 // one chain group per block: the producers make the next
                 // level's first round during this level's last one
                 const bool one_group = static_cast<size_t>(gridDim.x) * 32 >= a.chains_local;
-                e = pc_sweep<R, Cost, NT>(prow, n, a.family, e, temperature, static_cast<uint32_t>(a.chain_begin + g * 32),
-                                          static_cast<uint32_t>(l), ctr, a.N, box, a.keys, masks + cl, a.mask_stride,
-                                          live, pcbuf, pc_slot, one_group && pc_prefilled,
-                                          one_group && l + 1 < a.levels);
+                if constexpr (LZ)
+                    e = pc_sweep_lazy<R, Cost, NT>(prow, n, a.family, e, temperature,
+                                                   static_cast<uint32_t>(a.chain_begin + g * 32), static_cast<uint32_t>(l),
+                                                   ctr, a.N, box, a.keys, masks + cl, a.mask_stride, live, pcbuf, pc_slot,
+                                                   one_group && pc_prefilled, one_group && l + 1 < a.levels,
+                                                   static_cast<R>(a.lazy_r), static_cast<R>(a.lazy_alpha), st);
+                else
+                    e = pc_sweep<R, Cost, NT>(prow, n, a.family, e, temperature, static_cast<uint32_t>(a.chain_begin + g * 32),
+                                              static_cast<uint32_t>(l), ctr, a.N, box, a.keys, masks + cl, a.mask_stride,
+                                              live, pcbuf, pc_slot, one_group && pc_prefilled,
+                                              one_group && l + 1 < a.levels);
                 pc_prefilled = one_group && l + 1 < a.levels;
                 if (live) {
                     st.evals += static_cast<uint64_t>(a.N);
@@ -846,6 +941,12 @@ __global__ void __launch_bounds__(PSA_V2_MAX_THREADS, PSA_V2_MIN_BLOCKS) v2_lazy
     v2_body<R, Cost, NT, G, false, false, true, UB>(a);
 }
 
+// producer/consumer blocks with the deferred-fold consumer (pc_sweep_lazy)
+template <class R, class Cost, int NT>
+__global__ void __launch_bounds__(128, 4) v2_lazy_pc_kernel(const EngineArgs a) {
+    v2_body<R, Cost, NT, false, false, true, true>(a);
+}
+
 // producer/consumer blocks for small chain counts: warp 0 consumes, warps
 // 1..3 produce (pc_sweep)
 template <class R, class Cost, int NT>
@@ -1011,7 +1112,10 @@ __device__ void pc_produce_x(PcEntryX<R, Cost::A>* buf, long long j0, int jn, in
     }
 }
 
-template <class R, class Cost, int NT>
+// LZ: the consumer decides from the deferred-fold interval (sweep_lazy) and
+// folds only to settle and at level ends (engines.cpp:90-106 reads the
+// chain's energy there); v1_lazy_pc_kernel
+template <class R, class Cost, int NT, bool LZ = false>
 __global__ void __launch_bounds__(128, 4) v1_pc_kernel(const EngineArgs a) {
     constexpr int A = Cost::A;
     fn_param_init<Cost>(a.fparam);
@@ -1076,6 +1180,7 @@ __global__ void __launch_bounds__(128, 4) v1_pc_kernel(const EngineArgs a) {
         }
         if (live) st.evals += 1;
         double chain_best = static_cast<double>(e);
+        bool have = true; // LZ: e is the exact energy of the row
         if (producer) pc_produce_x<R, Cost>(buf, 0, total < 32 ? static_cast<int>(total) : 32, n, chain_base, ctr0, box, a.keys);
         __syncthreads();
         int level = 0, in_level = 0; // the trial's level and position in it
@@ -1095,7 +1200,47 @@ __global__ void __launch_bounds__(128, 4) v1_pc_kernel(const EngineArgs a) {
                 for (int j = 0; j < jn; ++j) {
                     const PcEntryX<R, A> en = nx;
                     nx = cur[(j + 1 < jn ? j + 1 : j) * 32 + lane];
-                    if (live) {
+                    if constexpr (LZ) {
+                        if (live) {
+                            using LF = LazyOf<typename Cost::Fam>;
+                            const R sa = LF::sigma > 0 ? static_cast<R>(a.lazy_alpha) : -static_cast<R>(a.lazy_alpha);
+                            const R rr = static_cast<R>(a.lazy_r);
+                            const R to = row[en.p.d];
+                            const MBand b = metropolis_band(en.p.m);
+                            const R q = (en.p.t[0] - to) * sa;
+                            const R hi = q + rr, lo = q - rr;
+                            int r = ((hi <= R(0)) | (static_cast<float>(hi) * k2 < b.lo))
+                                        ? 1
+                                        : (((lo > R(0)) & (static_cast<float>(lo) * k2 > b.hi)) ? 0 : -1);
+                            bool settled = false;
+                            if (__any_sync(__activemask(), r < 0)) {
+                                if (__any_sync(__activemask(), (r < 0) & !have)) {
+                                    const R eo = Cost::template energy<NT>(row, n, a.family);
+                                    if (!have) {
+                                        e = eo;
+                                        have = true;
+                                    }
+                                }
+                                if (r < 0) row[en.p.d] = en.p.t[0];
+                                const R et = Cost::template energy<NT>(row, n, a.family);
+                                if (r < 0) {
+                                    int v = metropolis_fast<R>(et, e, k2, b);
+                                    if (v < 0)
+                                        v = Accept<R>::exact(static_cast<double>(et) - static_cast<double>(e),
+                                                             a.temps[level], en.p.m);
+                                    if (v) e = et;
+                                    else row[en.p.d] = to;
+                                    r = v;
+                                    settled = true;
+                                }
+                            }
+                            if (r && !settled) {
+                                row[en.p.d] = en.p.t[0];
+                                have = false;
+                            }
+                            if (r) xrow[static_cast<size_t>(en.p.d) * xst] = en.x;
+                        }
+                    } else if (live) {
                         R to[A];
 #pragma unroll
                         for (int q = 0; q < A; ++q) {
@@ -1116,6 +1261,15 @@ __global__ void __launch_bounds__(128, 4) v1_pc_kernel(const EngineArgs a) {
                         }
                     }
                     if (++in_level == a.N) {
+                        if constexpr (LZ) { // the level-end energy is an exact fold
+                            if (__any_sync(0xffffffffu, live && !have)) {
+                                const R ef = Cost::template energy<NT>(row, n, a.family);
+                                if (live && !have) {
+                                    e = ef;
+                                    have = true;
+                                }
+                            }
+                        }
                         // level end (engines.cpp:90-106): std::min(chain_best, energy),
                         // then the warp's trace candidate (NaN skipped)
                         if (static_cast<double>(e) < chain_best) chain_best = static_cast<double>(e);
@@ -1397,6 +1551,8 @@ struct KernelSet {
         k.v2zu = nullptr;
         k.v2gz = nullptr;
         k.v2gzu = nullptr;
+        k.v2pcz = nullptr;
+        k.v1pcz = nullptr;
         k.v2pz = nullptr;
         k.lazy_radius = nullptr;
         k.lazy_alpha_of = nullptr;
@@ -1405,6 +1561,8 @@ struct KernelSet {
             k.v2zu = reinterpret_cast<const void*>(&v2_lazy_kernel<R, Cost, NT, false, true>);
             k.v2gz = reinterpret_cast<const void*>(&v2_lazy_kernel<R, Cost, 0, true>);
             k.v2gzu = reinterpret_cast<const void*>(&v2_lazy_kernel<R, Cost, 0, true, true>);
+            k.v2pcz = reinterpret_cast<const void*>(&v2_lazy_pc_kernel<R, Cost, NT>);
+            k.v1pcz = reinterpret_cast<const void*>(&v1_pc_kernel<R, Cost, NT, true>);
             k.lazy_radius = &LazyCost<Cost>::radius;
             k.lazy_alpha_of = &LazyCost<Cost>::alpha;
             if constexpr (PairOf<Cost>::value) k.v2pz = reinterpret_cast<const void*>(&v2_lazy_pair_kernel<R, Cost, NT>);

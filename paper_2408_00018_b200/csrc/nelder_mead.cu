@@ -47,6 +47,10 @@ using NMArgs = NMArgsHost;
 // centroid prefix sums are kept at positions 0, C, 2C, ... (P row p/C)
 constexpr int kNmCheckpoint = 16;
 
+// ranges of one introsort level over n+1 values (each larger than the
+// insertion threshold, so at most (n+1)/17 of them), with slack
+PSA_HD int nm_sort_ranges(int n) { return (n + 1) / 16 + 2; }
+
 __device__ __forceinline__ double clampd(double v, double lo, double hi) {
     return v < lo ? lo : (hi < v ? hi : v); // std::clamp
 }
@@ -66,40 +70,31 @@ __device__ __forceinline__ double clampd(double v, double lo, double hi) {
 // the termination test max-reduces CL partials through DSMEM.
 // ---------------------------------------------------------------------------
 
-// The exact introsort's task form on warp 0 (psa_sort::range_task: one lane
-// per disjoint range, level by level; see parsa_stdsort_pairs.hpp).  Range
-// lists: cur / nxt, 3 ints per range; *count: the next level's length.  Not
-// inlined: its registers would otherwise be charged to the whole NM kernel.
-static __device__ __noinline__ void exact_sort_tasks(psa_sort::KeyId* kp, int m, int* cur, int* nxt, int* count) {
-    const int lane = threadIdx.x & 31;
-    if (lane == 0) {
-        cur[0] = 0;
-        cur[1] = m;
-        cur[2] = psa_lg(m) * 2;
+// The centroid re-add of one column (nelder_mead.cpp:70-73 from the
+// checkpoint at vp): one dependent DADD chain in the reference's summation
+// order, so its cost is latency — whole checkpoint segments load their 16
+// quotients, then add unconditionally (no predicated selects in the chain;
+// the caller passes shared-memory pointers when Q lives there, so the loads
+// are LDS rather than generic loads).  Q element (v, 0) at
+// Qc[v * st], P row r at Pc[r * st]; writes the checkpoints it passes.
+static __device__ __forceinline__ double centroid_readd(const double* Qc, double* Pc, size_t st, const int* ord_s,
+                                                       int vp, int n) {
+    double c = Pc[static_cast<size_t>(vp / kNmCheckpoint) * st];
+    int p0 = vp;
+    for (; p0 + kNmCheckpoint <= n; p0 += kNmCheckpoint) {
+        double q[kNmCheckpoint];
+#pragma unroll
+        for (int i = 0; i < kNmCheckpoint; ++i) q[i] = Qc[static_cast<size_t>(ord_s[p0 + i]) * st];
+#pragma unroll
+        for (int i = 0; i < kNmCheckpoint; ++i) c += q[i];
+        Pc[static_cast<size_t>((p0 + kNmCheckpoint) / kNmCheckpoint) * st] = c;
     }
-    int cnt = 1;
-    __syncwarp();
-    while (cnt > 0) {
-        if (lane == 0) *count = 0;
-        __syncwarp();
-        for (int i = lane; i < cnt; i += 32)
-            psa_sort::range_task(kp, cur[3 * i], cur[3 * i + 1], cur[3 * i + 2], [&](int f, int l, int d) {
-                const int k = atomicAdd(count, 1);
-                nxt[3 * k] = f;
-                nxt[3 * k + 1] = l;
-                nxt[3 * k + 2] = d;
-            });
-        __syncwarp();
-        cnt = *count;
-        __syncwarp();
-        int* t = cur;
-        cur = nxt;
-        nxt = t;
-    }
+    for (; p0 < n; ++p0) c += Qc[static_cast<size_t>(ord_s[p0]) * st]; // the last, partial segment
+    return c;
 }
 
 template <class Cost>
-__global__ void __launch_bounds__(512) nm_kernel(const NMArgs a) {
+__global__ void __launch_bounds__(512, 1) nm_kernel(const NMArgs a) {
     constexpr int A = Cost::A;
     fn_param_init<Cost>(a.fparam);
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -157,7 +152,9 @@ __global__ void __launch_bounds__(512) nm_kernel(const NMArgs a) {
     // memory when the slice fits (a.q_smem), else in global memory.  Element
     // (v, j) of either lives at base[v * stride + j].
     // (the shared slice starts after the int scratch: ist[4], ranks, saved order)
-    const uintptr_t qraw = (reinterpret_cast<uintptr_t>(ist + 4 + 2 * (n + 1)) + 15) & ~uintptr_t(15);
+    const int nranges = nm_sort_ranges(n); // range lists of the warp exact sort
+    const uintptr_t qraw =
+        (reinterpret_cast<uintptr_t>(ist + 4 + 2 * (n + 1) + 10 * nranges) + 15) & ~uintptr_t(15);
     double* Qb = a.q_smem ? reinterpret_cast<double*>(qraw) : a.Q + c0;
     const size_t qst = a.q_smem ? static_cast<size_t>(ncmax) : static_cast<size_t>(n);
     double* Pb = a.q_smem ? Qb + static_cast<size_t>(n + 1) * ncmax : a.P + c0;
@@ -272,6 +269,9 @@ __global__ void __launch_bounds__(512) nm_kernel(const NMArgs a) {
     // order, so the block runs that exact algorithm (parsa_stdsort.h).
     int* rk = ist + 4;         // n+1 ints: ranks of the full sort
     int* saved = rk + (n + 1); // n+1 ints: the pre-sort order
+    // the warp exact sort: rk / saved hold its stop lists, these its ranges
+    const psa_sort::WarpSortLists wsl{saved + (n + 1), saved + (n + 1) + 3 * nranges,
+                                      saved + (n + 1) + 6 * nranges};
     auto equiv = [](double a, double b) { return !(a < b) && !(b < a); };
     // (key, id) pairs for the exact sort: one 16-byte load per comparison
     // instead of an id and then its key (the terms area is idle here)
@@ -300,7 +300,7 @@ __global__ void __launch_bounds__(512) nm_kernel(const NMArgs a) {
         if (__syncthreads_or(has_nan) || n + 1 <= PSA_SORT_THRESHOLD) {
             if (tid == 0) psa_sort::sort(kp, n + 1);
         } else if (tid < 32) {
-            exact_sort_tasks(kp, n + 1, rk, saved, &ist[2]);
+            psa_sort::warp_sort(kp, n + 1, rk, saved, wsl);
         }
         __syncthreads();
         const int old_best = ord_s[0];
@@ -454,23 +454,20 @@ __global__ void __launch_bounds__(512) nm_kernel(const NMArgs a) {
         // sums are stored every kNmCheckpoint positions)
         const int vp = (ist[0] / kNmCheckpoint) * kNmCheckpoint;
         NMC(2, n - vp);
-        for (int j = tid; j < nc; j += B) {
-            double c = Pb[static_cast<size_t>(vp / kNmCheckpoint) * qst + j];
-            // one checkpoint segment at a time: its (up to 16) quotients are
-            // loaded first, so the loads overlap each other instead of each
-            // add waiting for its own load
-            for (int p0 = vp; p0 < n; p0 += kNmCheckpoint) {
-                const int m = n - p0 < kNmCheckpoint ? n - p0 : kNmCheckpoint;
-                double q[kNmCheckpoint];
-#pragma unroll
-                for (int i = 0; i < kNmCheckpoint; ++i)
-                    if (i < m) q[i] = Qb[static_cast<size_t>(ord_s[p0 + i]) * qst + j];
-#pragma unroll
-                for (int i = 0; i < kNmCheckpoint; ++i)
-                    if (i < m) c += q[i];
-                if (m == kNmCheckpoint) Pb[static_cast<size_t>((p0 + m) / kNmCheckpoint) * qst + j] = c;
-            }
-            cen[j] = c;
+        // The re-add is one dependent DADD chain per column (the reference's
+        // summation order), so its cost is latency: whole checkpoint segments
+        // add unconditionally (no predicated selects in the chain), the next
+        // segment's quotients are loaded while this one adds, and with Q in
+        // shared memory the loads are LDS (the branch keeps the pointer's
+        // address space visible to the compiler).
+        if (a.q_smem) {
+            const double* Qs = reinterpret_cast<const double*>(qraw);
+            double* Ps = reinterpret_cast<double*>(qraw) + static_cast<size_t>(n + 1) * ncmax;
+            for (int j = tid; j < nc; j += B)
+                cen[j] = centroid_readd(Qs + j, Ps + j, static_cast<size_t>(ncmax), ord_s, vp, n);
+        } else {
+            for (int j = tid; j < nc; j += B)
+                cen[j] = centroid_readd(a.Q + c0 + j, a.P + c0 + j, static_cast<size_t>(n), ord_s, vp, n);
         }
         __syncthreads();
         if (tid == 0) ist[0] = n;
@@ -696,11 +693,12 @@ const void* nm_batch_kernel_for(int family) {
 // checkpoints (n/16+1 rows) in shared memory
 size_t nm_smem_bytes(int n, int cl, bool q_smem) {
     const size_t nc = (static_cast<size_t>(n) + cl - 1) / cl;
+    const size_t ranges = static_cast<size_t>(nm_sort_ranges(n));
     // doubles: terms (2n + 8), own-column cen/xr/xe/xc (4 nc), red/scal/dslot
     // (56), f and D (2(n+1)); ints: order, ranks, saved order (3(n+1)) and
     // scalars (4), padding (2)
     size_t b = sizeof(double) * (2 * static_cast<size_t>(n) + 8 + 4 * nc + 56 + 2 * (static_cast<size_t>(n) + 1)) +
-               sizeof(int) * (3 * (static_cast<size_t>(n) + 1) + 6);
+               sizeof(int) * (3 * (static_cast<size_t>(n) + 1) + 6 + 10 * ranges);
     b = (b + 15) & ~size_t(15);
     if (q_smem) b += sizeof(double) * nc * (static_cast<size_t>(n) + 1 + static_cast<size_t>(n) / kNmCheckpoint + 1);
     return b + 64;

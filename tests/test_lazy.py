@@ -23,12 +23,14 @@ from test_gpu_parity import device_run
 
 pytestmark = pytest.mark.gpu
 
-@pytest.fixture(autouse=True, params=["lazy1", "lazypair"])
+@pytest.fixture(autouse=True, params=["lazy1", "lazypair", "lazypc"])
 def _lazy_kernel(request, monkeypatch):
-    """small chain counts default to the producer/consumer kernel; these
-    tests pin the deferred-fold kernels: one chain per thread (lazy1) and
-    chain pairs (lazypair; binary32 only — f64 plans fall back to lazy1)"""
+    """these tests pin each deferred-fold kernel: one chain per thread
+    (lazy1), chain pairs (lazypair; binary32 only — f64 plans fall back to
+    lazy1) and the producer/consumer blocks with the deferred-fold consumer
+    (lazypc, the default at small chain counts)"""
     monkeypatch.setenv("PSA_V2_MODE", request.param)
+    return request.param
 
 
 LAZY = [("SCHWEFEL", -512.0, 512.0), ("RASTRIGIN", -5.12, 5.12), ("SPHERE", -2.0, 2.0),
@@ -140,9 +142,11 @@ def test_metropolis_pretest_never_contradicts_the_exact_test(gpu_lib, prec):
 
 
 @pytest.mark.parametrize("prec", [0, 1])
-def test_large_n_lazy_hbm_rows_match_oracle(gpu_lib, prec):
+def test_large_n_lazy_hbm_rows_match_oracle(gpu_lib, _lazy_kernel, prec):
     """n = 500 (C4's SA phase): the deferred fold keeps its rows in HBM
     (shared-memory rows would leave 3 warps per SM)."""
+    if _lazy_kernel == "lazypc":
+        pytest.skip("the producer/consumer kernel keeps its 32 rows in shared memory")
     prob = Problem("SCHWEFEL", 500, -512.0, 512.0)
     sched = (1000.0, 100.0, 0.5, 100)  # warm: binary32 keeps HBM rows only above rr * n
     cfg = Config(64, sched, 8, prec, 1)
@@ -166,3 +170,20 @@ def test_large_n_lazy_equals_fold_every_trial(gpu_lib, monkeypatch, prec):
         full = device_run(2, prob, cfg)
         monkeypatch.delenv("PSA_LAZY")
         assert not same_run(lazy, full), (sched, same_run(lazy, full))
+
+
+@pytest.mark.parametrize("family,lo,hi", LAZY)
+@pytest.mark.parametrize("prec", [0, 1])
+def test_v1_and_v0_lazy_consumer_match_oracle(gpu_lib, monkeypatch, family, lo, hi, prec):
+    """The asynchronous engine's producer/consumer kernel with the deferred-
+    fold consumer (v1_lazy_pc_kernel): level-end energies are exact folds
+    (engines.cpp:90-106), every decision the reference's.  Also V0
+    (run_sequential = one chain, engines.cpp:125-129)."""
+    monkeypatch.setenv("PSA_V2_MODE", "lazypc")
+    from oracle_lib import oracle_async
+    prob = Problem(family, 30, lo, hi)
+    for engine, chains, start in ((1, 333, 1), (1, 64, 0), (0, 1, 0)):
+        cfg = Config(chains, (20.0, 0.002, 0.6, 50), 17, prec, start)
+        got = device_run(engine, prob, cfg)
+        want = oracle_async(prob, cfg)
+        assert not same_run(got, want), (engine, chains, same_run(got, want))
