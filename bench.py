@@ -18,10 +18,12 @@ rho=0.99, N=100 (1146 levels), precision f32 (the paper's default).  One
   cpu_baseline  the reference's own CPU implementation (oracle/_ref, all host
              threads) on a bounded sample of the same workload
 
-Multi-GPU (torchrun, N>1): weak scaling, 2^20 chains per GPU of one global
-synchronous run (global stream keys); the per-level minloc is exchanged
-inside the persistent kernel through peer-mapped mailboxes over NVLink
-(paper_2408_00018_b200/dist.py, engine.cu exchange_level).
+Multi-GPU (torchrun, N>1): configs[4] — 2^23 chains of one global
+synchronous run sharded over the N GPUs (strong scaling; global stream
+keys, so the result equals the 1-GPU run of the same chains); the per-level
+minloc is exchanged inside the persistent kernel through peer-mapped
+mailboxes over NVLink (paper_2408_00018_b200/dist.py, exchange_level).
+`--chains N` keeps N chains per GPU instead (weak scaling).
 
 `--impl reference` runs only the reference CPU arm and prints its line.
 """
@@ -401,6 +403,9 @@ def main():
         raise SystemExit("bench: no sm_100 device visible (the library has no CPU fallback)")
 
     prec = psa.Precision.f32 if args.precision == "f32" else psa.Precision.f64
+    if world > 1 and args.chains_total == 0 and args.chains == CHAINS_PER_GPU:
+        # BASELINE.json configs[4]: 2^23 chains sharded across 2/4/8 GPUs
+        args.chains_total = 1 << 23
     if args.chains_total > 0:  # strong scaling: a fixed global run sharded over the GPUs
         from paper_2408_00018_b200.dist import shard_range
 

@@ -578,6 +578,9 @@ PSA_DEV R sweep_lazy(Row row, int n_rt, int family, R E, double temperature, uin
         q2 = draw_bits53_fast(ctr + 4, pc, keys);
         q3 = draw_bits53_fast(ctr + 5, pc, keys);
     }
+#ifdef PSA_P0_ADD
+    uint64_t p6 = static_cast<uint64_t>(kPhiloxM0) * (ctr + 6); // M0 * (counter of the next draw batch)
+#endif
     // the cached term a trial replaces is loaded one trial ahead (HBM rows:
     // the load latency overlaps the previous trial)
     R to = row[d];
@@ -592,9 +595,17 @@ PSA_DEV R sweep_lazy(Row row, int n_rt, int family, R E, double temperature, uin
             R tnn[1];
             bool ok;
             Cost::cache_common(static_cast<R>(xn), dn, n, tnn, ok);
+#ifdef PSA_P0_ADD
+            // first-round products by addition (draw_bits53_p0)
+            const uint64_t r1 = draw_bits53_p0(p6, pc, keys);
+            const uint64_t r2 = draw_bits53_p0(p6 + kPhiloxM0, pc, keys);
+            const uint64_t r3 = draw_bits53_p0(p6 + 2ull * kPhiloxM0, pc, keys);
+            p6 += 3ull * kPhiloxM0;
+#else
             const uint64_t r1 = draw_bits53_fast(ctr + 6, pc, keys);
             const uint64_t r2 = draw_bits53_fast(ctr + 7, pc, keys);
             const uint64_t r3 = draw_bits53_fast(ctr + 8, pc, keys);
+#endif
             const MBand b3 = metropolis_band(m3);
             // the interval decision
             const R q = (tn[0] - to) * sa;
