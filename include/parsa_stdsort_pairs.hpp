@@ -351,7 +351,26 @@ __device__ inline void warp_adjust_heap(KeyId* v, int first, int hole, int len, 
     __syncwarp();
 }
 
-__device__ inline void warp_heap_sort(KeyId* v, int first, int last) {
+// ascending sort of [first, last) in place, for DISTINCT keys (any correct
+// sort gives the same order then): odd-even transposition, one compare-
+// exchange per lane per phase
+__device__ inline void warp_sort_distinct(KeyId* v, int first, int last) {
+    const int lane = threadIdx.x & 31;
+    const int m = last - first;
+    for (int phase = 0; phase < m; ++phase) {
+        for (int i = first + (phase & 1) + 2 * lane; i + 1 < last; i += 64)
+            if (less(v[i + 1], v[i])) swap(v, i, i + 1);
+        __syncwarp();
+    }
+}
+
+// heap_sort of [first, last).  tie_min: the smallest key that occurs more
+// than once in the whole array (+inf: none).  sort_heap pops the maximum
+// each step, so once the root is below tie_min every remaining key is
+// distinct and their heapsort order is simply ascending: the pops stop there
+// and the rest is sorted directly — the same result, without the pops whose
+// order no tie can observe.
+__device__ inline void warp_heap_sort(KeyId* v, int first, int last, double tie_min) {
     const int lane = threadIdx.x & 31;
     const int len = last - first;
     if (len >= 2) {
@@ -365,7 +384,7 @@ __device__ inline void warp_heap_sort(KeyId* v, int first, int last) {
             __syncwarp();
         }
     }
-    while (last - first > 1) {
+    while (last - first > 1 && !(v[first].key < tie_min)) {
         --last;
         const KeyId value = v[last];
         __syncwarp();
@@ -373,9 +392,11 @@ __device__ inline void warp_heap_sort(KeyId* v, int first, int last) {
         __syncwarp();
         warp_adjust_heap(v, first, 0, last - first, value);
     }
+    if (last - first > 1) warp_sort_distinct(v, first, last);
 }
 
-__device__ inline void warp_sort(KeyId* v, int m, int* ls, int* rs, WarpSortLists L) {
+__device__ inline void warp_sort(KeyId* v, int m, int* ls, int* rs, WarpSortLists L,
+                                 double tie_min = __builtin_huge_val()) {
     const int lane = threadIdx.x & 31;
     if (m <= PSA_SORT_THRESHOLD) {
         if (lane == 0) insertion_sort(v, 0, m);
@@ -396,7 +417,7 @@ __device__ inline void warp_sort(KeyId* v, int m, int* ls, int* rs, WarpSortList
         for (int r = 0; r < nc; ++r) {
             const int f = cur[3 * r], l = cur[3 * r + 1], d = cur[3 * r + 2];
             if (d == 0) {
-                warp_heap_sort(v, f, l);
+                warp_heap_sort(v, f, l, tie_min);
                 continue;
             }
             if (lane == 0) median_to_first(v, f, f + 1, f + (l - f) / 2, l - 1);

@@ -6,8 +6,19 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <algorithm>
 #include <cstdlib>
+#include <cmath>
 #include <vector>
+
+// the smallest key occurring more than once (+inf: none)
+static double tie_min_of(const std::vector<double>& k, int m) {
+    std::vector<double> s(k.begin(), k.begin() + m);
+    std::sort(s.begin(), s.end());
+    for (int i = 0; i + 1 < m; ++i)
+        if (s[i] == s[i + 1]) return s[i];
+    return INFINITY;
+}
 
 #include "parsa_stdsort.h"
 #include "parsa_stdsort_pairs.hpp"
@@ -46,7 +57,7 @@ __global__ void heap_kernel(int m, int pf, long long* cyc) {
     if (lane == 0) { cyc[0] = t1 - t0; cyc[1] = t2 - t1; }
 }
 
-__global__ void sort_kernel(const double* keys, int m, int* out_ids, long long* cyc) {
+__global__ void sort_kernel(const double* keys, int m, int* out_ids, long long* cyc, double tie_min) {
     __shared__ psa_sort::KeyId kp[1024];
     __shared__ int ls[1024], rs[1024], lists[10 * 80];
     const int lane = threadIdx.x;
@@ -54,7 +65,7 @@ __global__ void sort_kernel(const double* keys, int m, int* out_ids, long long* 
     __syncwarp();
     const psa_sort::WarpSortLists L{lists, lists + 3 * 80, lists + 6 * 80};
     const long long t0 = clock64();
-    psa_sort::warp_sort(kp, m, ls, rs, L);
+    psa_sort::warp_sort(kp, m, ls, rs, L, tie_min);
     const long long t1 = clock64();
     for (int p = lane; p < m; p += 32) out_ids[p] = kp[p].id;
     if (lane == 0) *cyc = t1 - t0;
@@ -82,7 +93,7 @@ int main() {
             for (int p = 0; p < m - 1; ++p) keys[p] = s[p].key;
         }
         cudaMemcpy(dk, keys.data(), m * sizeof(double), cudaMemcpyHostToDevice);
-        sort_kernel<<<1, 32>>>(dk, m, di, dc);
+        sort_kernel<<<1, 32>>>(dk, m, di, dc, t % 2 ? tie_min_of(keys, m) : INFINITY);
         cudaMemcpy(got.data(), di, m * sizeof(int), cudaMemcpyDeviceToHost);
         std::vector<psa_sort::KeyId> want(m);
         for (int p = 0; p < m; ++p) want[p] = psa_sort::KeyId{keys[p], p, 0};
@@ -104,7 +115,7 @@ int main() {
                       : mode == 2 ? 1.0 : (p < m - 1 ? p / 5 : 50.0);
         }
         cudaMemcpy(dk, keys.data(), m * sizeof(double), cudaMemcpyHostToDevice);
-        sort_kernel<<<1, 32>>>(dk, m, di, dc);
+        sort_kernel<<<1, 32>>>(dk, m, di, dc, tie_min_of(keys, m));
         long long c;
         cudaMemcpy(&c, dc, sizeof(c), cudaMemcpyDeviceToHost);
         std::printf("{\"input\": \"%s\", \"m\": 501, \"cycles\": %lld}\n", names[mode], c);
