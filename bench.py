@@ -240,8 +240,10 @@ def _smem_peak():
 # multiplies; for a fixed (chain, level) the chain and level words make the
 # first-round product of word 2 and the second-round product of word 0
 # invariants, and the last round needs one product only: 17 mulhilo per
-# draw, 51 per trial (philox.cuh, draw_bits53_fast).
-PHILOX_MULHILO_PER_TRIAL = 51
+# draw; the first-round product of the counter word is linear in the
+# counter, so consecutive draws get it by a 64-bit add (draw_bits53_p0):
+# 16 per draw, 48 per trial.
+PHILOX_MULHILO_PER_TRIAL = 48
 
 
 def kernel_roofline(desc, dim, bytes_per_coord, trials, seconds):

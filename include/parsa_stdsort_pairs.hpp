@@ -352,20 +352,46 @@ __device__ inline void warp_adjust_heap(KeyId* v, int first, int hole, int len, 
 }
 
 // ascending sort of [first, last) in place, for DISTINCT keys (any correct
-// sort gives the same order then): odd-even transposition, one compare-
-// exchange per lane per phase
+// sort gives the same order then): the bitonic network in its all-ascending
+// form (each merge starts by comparing every position with its mirror in the
+// block), padded to a power of two with positions that act as +inf — with
+// every comparator putting the smaller key first, a real element never moves
+// into the padding
 __device__ inline void warp_sort_distinct(KeyId* v, int first, int last) {
     const int lane = threadIdx.x & 31;
     const int m = last - first;
-    for (int phase = 0; phase < m; ++phase) {
-        for (int i = first + (phase & 1) + 2 * lane; i + 1 < last; i += 64)
-            if (less(v[i + 1], v[i])) swap(v, i, i + 1);
+    int P = 1;
+    while (P < m) P <<= 1;
+    KeyId* b = v + first;
+    auto cmpx = [&](int i, int l) { // i < l
+        if (l < m) {
+            const KeyId x = b[i], y = b[l];
+            if (less(y, x)) {
+                b[i] = y;
+                b[l] = x;
+            }
+        }
+    };
+    for (int k = 2; k <= P; k <<= 1) {
+        const int h = k >> 1;
+        for (int t = lane; t < P / 2; t += 32) {
+            const int blk = t / h, w = t - blk * h;
+            cmpx(blk * k + w, blk * k + k - 1 - w);
+        }
         __syncwarp();
+        for (int j = k >> 2; j > 0; j >>= 1) {
+            for (int t = lane; t < P / 2; t += 32) {
+                const int i = ((t & ~(j - 1)) << 1) | (t & (j - 1));
+                cmpx(i, i | j);
+            }
+            __syncwarp();
+        }
     }
 }
 
 // heap_sort of [first, last).  tie_min: the smallest key that occurs more
-// than once in the whole array (+inf: none).  sort_heap pops the maximum
+// than once in the whole array (+inf: none; -inf, the default of warp_sort:
+// unknown — every pop runs).  sort_heap pops the maximum
 // each step, so once the root is below tie_min every remaining key is
 // distinct and their heapsort order is simply ascending: the pops stop there
 // and the rest is sorted directly — the same result, without the pops whose
@@ -396,7 +422,7 @@ __device__ inline void warp_heap_sort(KeyId* v, int first, int last, double tie_
 }
 
 __device__ inline void warp_sort(KeyId* v, int m, int* ls, int* rs, WarpSortLists L,
-                                 double tie_min = __builtin_huge_val()) {
+                                 double tie_min = -__builtin_huge_val()) {
     const int lane = threadIdx.x & 31;
     if (m <= PSA_SORT_THRESHOLD) {
         if (lane == 0) insertion_sort(v, 0, m);

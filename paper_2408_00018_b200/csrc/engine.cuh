@@ -578,7 +578,7 @@ PSA_DEV R sweep_lazy(Row row, int n_rt, int family, R E, double temperature, uin
         q2 = draw_bits53_fast(ctr + 4, pc, keys);
         q3 = draw_bits53_fast(ctr + 5, pc, keys);
     }
-#ifdef PSA_P0_ADD
+#ifndef PSA_P0_MUL
     uint64_t p6 = static_cast<uint64_t>(kPhiloxM0) * (ctr + 6); // M0 * (counter of the next draw batch)
 #endif
     // the cached term a trial replaces is loaded one trial ahead (HBM rows:
@@ -595,7 +595,7 @@ PSA_DEV R sweep_lazy(Row row, int n_rt, int family, R E, double temperature, uin
             R tnn[1];
             bool ok;
             Cost::cache_common(static_cast<R>(xn), dn, n, tnn, ok);
-#ifdef PSA_P0_ADD
+#ifndef PSA_P0_MUL
             // first-round products by addition (draw_bits53_p0)
             const uint64_t r1 = draw_bits53_p0(p6, pc, keys);
             const uint64_t r2 = draw_bits53_p0(p6 + kPhiloxM0, pc, keys);

@@ -93,7 +93,7 @@ int main() {
             for (int p = 0; p < m - 1; ++p) keys[p] = s[p].key;
         }
         cudaMemcpy(dk, keys.data(), m * sizeof(double), cudaMemcpyHostToDevice);
-        sort_kernel<<<1, 32>>>(dk, m, di, dc, t % 2 ? tie_min_of(keys, m) : INFINITY);
+        sort_kernel<<<1, 32>>>(dk, m, di, dc, t % 2 ? tie_min_of(keys, m) : -INFINITY);
         cudaMemcpy(got.data(), di, m * sizeof(int), cudaMemcpyDeviceToHost);
         std::vector<psa_sort::KeyId> want(m);
         for (int p = 0; p < m; ++p) want[p] = psa_sort::KeyId{keys[p], p, 0};
