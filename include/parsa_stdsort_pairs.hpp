@@ -327,6 +327,7 @@ __device__ inline void warp_adjust_heap(KeyId* v, int first, int hole, int len, 
             s = ((second + 1) << k) - 1 + oo;
             depth = k;
         }
+        __syncwarp(); // every lane's load precedes any store (racecheck)
         // moves: chosen node at depth k goes to its parent's place (the hole
         // for k = 1); lanes holding chosen nodes store in parallel
 #pragma unroll

@@ -161,11 +161,13 @@ struct PcEntry {
 // buf[trial][lane], filled by threads 32.. of the block
 template <class R, class Cost>
 __device__ void pc_produce(PcEntry<R, Cost::A>* buf, int j0, int jn, int n, uint32_t chain_base, uint32_t level,
-                           uint32_t ctr0, const Box& box, const PhiloxKeys& keys) {
+                           uint32_t ctr0, const Box& box, const PhiloxKeys& keys, int lanes = 32) {
+    // (lanes: the group's live chains — a short last group, or V0's single
+    // chain, gets no entries for lanes that have no chain)
     const int p = static_cast<int>(threadIdx.x) - 32, np = static_cast<int>(blockDim.x) - 32;
     const double idx_scale = static_cast<double>(n) * 0x1.0p-53;
-    for (int e = p; e < 32 * jn; e += np) {
-        const int lane = e & 31, jj = e >> 5;
+    for (int e = p; e < lanes * jn; e += np) {
+        const int jj = e / lanes, lane = e - jj * lanes;
         const PhiloxChain pc = philox_chain(chain_base + lane, level, keys);
         const uint32_t ctr = ctr0 + 3u * static_cast<uint32_t>(j0 + jj);
         const uint64_t m1 = draw_bits53_fast(ctr, pc, keys);
@@ -191,7 +193,7 @@ template <class R, class Cost, int NT>
 __device__ R pc_sweep(R* row, int n_rt, int family, R E, double temperature, uint32_t chain_base, uint32_t level,
                       uint32_t ctr0, int N, const Box& box, const PhiloxKeys& keys, uint32_t* mask,
                       size_t mask_stride, bool live, PcEntry<R, Cost::A>* buf, int& slot, bool prefilled,
-                      bool prefetch_next) {
+                      bool prefetch_next, int lanes = 32) {
     constexpr int A = Cost::A;
     const int n = NT > 0 ? NT : n_rt;
     const float k2 = metropolis_k2(temperature); // log2(e) / T
@@ -200,7 +202,7 @@ __device__ R pc_sweep(R* row, int n_rt, int family, R E, double temperature, uin
     const int rounds = (N + 31) / 32;
     auto at = [&](int k) { return buf + ((slot + k) % 3) * 1024; }; // ring slot of round k
     if (!prefilled) {
-        if (producer) pc_produce<R, Cost>(at(0), 0, N < 32 ? N : 32, n, chain_base, level, ctr0, box, keys);
+        if (producer) pc_produce<R, Cost>(at(0), 0, N < 32 ? N : 32, n, chain_base, level, ctr0, box, keys, lanes);
         __syncthreads();
     }
     const bool short_last = rounds > 1 && N - 32 * (rounds - 1) <= 16;
@@ -209,11 +211,12 @@ __device__ R pc_sweep(R* row, int n_rt, int family, R E, double temperature, uin
         if (producer) {
             if (k + 1 < rounds) {
                 const int j1 = 32 * (k + 1);
-                pc_produce<R, Cost>(at(k + 1), j1, N - j1 < 32 ? N - j1 : 32, n, chain_base, level, ctr0, box, keys);
+                pc_produce<R, Cost>(at(k + 1), j1, N - j1 < 32 ? N - j1 : 32, n, chain_base, level, ctr0, box, keys,
+                                    lanes);
             }
             const bool early = short_last && k + 2 == rounds, late = !short_last && k + 1 == rounds;
             if (prefetch_next && (early || late))
-                pc_produce<R, Cost>(at(rounds), 0, N < 32 ? N : 32, n, chain_base, level + 1, 0u, box, keys);
+                pc_produce<R, Cost>(at(rounds), 0, N < 32 ? N : 32, n, chain_base, level + 1, 0u, box, keys, lanes);
         } else if (live) {
             const PcEntry<R, A>* cur = at(k);
             uint32_t word = 0;
@@ -258,7 +261,7 @@ template <class R, class Cost, int NT>
 __device__ R pc_sweep_lazy(R* row, int n_rt, int family, R E, double temperature, uint32_t chain_base,
                            uint32_t level, uint32_t ctr0, int N, const Box& box, const PhiloxKeys& keys,
                            uint32_t* mask, size_t mask_stride, bool live, PcEntry<R, Cost::A>* buf, int& slot,
-                           bool prefilled, bool prefetch_next, R rr, R alpha, SweepStats& st) {
+                           bool prefilled, bool prefetch_next, R rr, R alpha, SweepStats& st, int lanes = 32) {
     using L = LazyOf<typename Cost::Fam>;
     static_assert(Cost::A == 1, "deferred fold: one accumulator");
     const int n = NT > 0 ? NT : n_rt;
@@ -270,7 +273,7 @@ __device__ R pc_sweep_lazy(R* row, int n_rt, int family, R E, double temperature
     bool have = true;
     auto at = [&](int k) { return buf + ((slot + k) % 3) * 1024; };
     if (!prefilled) {
-        if (producer) pc_produce<R, Cost>(at(0), 0, N < 32 ? N : 32, n, chain_base, level, ctr0, box, keys);
+        if (producer) pc_produce<R, Cost>(at(0), 0, N < 32 ? N : 32, n, chain_base, level, ctr0, box, keys, lanes);
         __syncthreads();
     }
     const bool short_last = rounds > 1 && N - 32 * (rounds - 1) <= 16;
@@ -279,11 +282,12 @@ __device__ R pc_sweep_lazy(R* row, int n_rt, int family, R E, double temperature
         if (producer) {
             if (k + 1 < rounds) {
                 const int j1 = 32 * (k + 1);
-                pc_produce<R, Cost>(at(k + 1), j1, N - j1 < 32 ? N - j1 : 32, n, chain_base, level, ctr0, box, keys);
+                pc_produce<R, Cost>(at(k + 1), j1, N - j1 < 32 ? N - j1 : 32, n, chain_base, level, ctr0, box, keys,
+                                    lanes);
             }
             const bool early = short_last && k + 2 == rounds, late = !short_last && k + 1 == rounds;
             if (prefetch_next && (early || late))
-                pc_produce<R, Cost>(at(rounds), 0, N < 32 ? N : 32, n, chain_base, level + 1, 0u, box, keys);
+                pc_produce<R, Cost>(at(rounds), 0, N < 32 ? N : 32, n, chain_base, level + 1, 0u, box, keys, lanes);
         } else if (live) {
             const PcEntry<R, 1>* cur = at(k);
             uint32_t word = 0;
@@ -575,6 +579,7 @@ __device__ __forceinline__ void v2_body(const EngineArgs& a) {
             for (size_t g = blockIdx.x; g * 32 < a.chains_local; g += gridDim.x) {
                 const size_t cl = g * 32 + lane;
                 const bool live = consumer && cl < a.chains_local;
+                const int glanes = static_cast<int>(a.chains_local - g * 32 < 32 ? a.chains_local - g * 32 : 32);
                 const uint32_t c = static_cast<uint32_t>(a.chain_begin + (cl < a.chains_local ? cl : g * 32));
                 R* prow = V + static_cast<size_t>(lane) * S;
                 R e = 0;
@@ -606,12 +611,12 @@ __device__ __forceinline__ void v2_body(const EngineArgs& a) {
                                                    static_cast<uint32_t>(a.chain_begin + g * 32), static_cast<uint32_t>(l),
                                                    ctr, a.N, box, a.keys, masks + cl, a.mask_stride, live, pcbuf, pc_slot,
                                                    one_group && pc_prefilled, one_group && l + 1 < a.levels,
-                                                   static_cast<R>(a.lazy_r), static_cast<R>(a.lazy_alpha), st);
+                                                   static_cast<R>(a.lazy_r), static_cast<R>(a.lazy_alpha), st, glanes);
                 else
                     e = pc_sweep<R, Cost, NT>(prow, n, a.family, e, temperature, static_cast<uint32_t>(a.chain_begin + g * 32),
                                               static_cast<uint32_t>(l), ctr, a.N, box, a.keys, masks + cl, a.mask_stride,
                                               live, pcbuf, pc_slot, one_group && pc_prefilled,
-                                              one_group && l + 1 < a.levels);
+                                              one_group && l + 1 < a.levels, glanes);
                 pc_prefilled = one_group && l + 1 < a.levels;
                 if (live) {
                     st.evals += static_cast<uint64_t>(a.N);
@@ -1092,11 +1097,11 @@ struct PcEntryX {
 
 template <class R, class Cost>
 __device__ void pc_produce_x(PcEntryX<R, Cost::A>* buf, long long j0, int jn, int n, uint32_t chain_base,
-                             uint32_t ctr0, const Box& box, const PhiloxKeys& keys) {
+                             uint32_t ctr0, const Box& box, const PhiloxKeys& keys, int lanes = 32) {
     const int p = static_cast<int>(threadIdx.x) - 32, np = static_cast<int>(blockDim.x) - 32;
     const double idx_scale = static_cast<double>(n) * 0x1.0p-53;
-    for (int e = p; e < 32 * jn; e += np) {
-        const int lane = e & 31, jj = e >> 5;
+    for (int e = p; e < lanes * jn; e += np) {
+        const int jj = e / lanes, lane = e - jj * lanes;
         const PhiloxChain pc = philox_chain(chain_base + lane, 0u, keys);
         const uint32_t ctr = ctr0 + 3u * static_cast<uint32_t>(j0 + jj);
         const uint64_t m1 = draw_bits53_fast(ctr, pc, keys);
@@ -1181,7 +1186,10 @@ __global__ void __launch_bounds__(128, 4) v1_pc_kernel(const EngineArgs a) {
         if (live) st.evals += 1;
         double chain_best = static_cast<double>(e);
         bool have = true; // LZ: e is the exact energy of the row
-        if (producer) pc_produce_x<R, Cost>(buf, 0, total < 32 ? static_cast<int>(total) : 32, n, chain_base, ctr0, box, a.keys);
+        const int glanes = static_cast<int>(a.chains_local - g * 32 < 32 ? a.chains_local - g * 32 : 32);
+        if (producer)
+            pc_produce_x<R, Cost>(buf, 0, total < 32 ? static_cast<int>(total) : 32, n, chain_base, ctr0, box, a.keys,
+                                  glanes);
         __syncthreads();
         int level = 0, in_level = 0; // the trial's level and position in it
         float k2 = metropolis_k2(a.temps[0]);
@@ -1192,7 +1200,7 @@ __global__ void __launch_bounds__(128, 4) v1_pc_kernel(const EngineArgs a) {
                 if (k + 1 < rounds) {
                     const long long j1 = j0 + 32;
                     pc_produce_x<R, Cost>(buf + ((k + 1) & 1) * 1024, j1, total - j1 < 32 ? static_cast<int>(total - j1) : 32,
-                                          n, chain_base, ctr0, box, a.keys);
+                                          n, chain_base, ctr0, box, a.keys, glanes);
                 }
             } else {
                 const PcEntryX<R, A>* cur = buf + (k & 1) * 1024;
