@@ -415,7 +415,11 @@ void plan_build(psa_plan* p, const psa_objective* f, const psa_engine_config* cf
         smem_pc <= smem_cap) {
         p->pc = true;
         p->lazy_pc = lazy_pc;
-        p->block = B = 128;
+        // one chain group (32 chains) per block; when the groups do not fill
+        // the SMs (C1: 32 groups), seven producer warps per block instead of
+        // three (the producers bound the deferred-fold consumer)
+        const long long groups = (static_cast<long long>(p->chains_local) + 31) / 32;
+        p->block = B = groups <= lim.sms ? 256 : 128;
         p->smem = smem_pc;
         kern = pc_kern;
     }

@@ -948,14 +948,14 @@ __global__ void __launch_bounds__(PSA_V2_MAX_THREADS, PSA_V2_MIN_BLOCKS) v2_lazy
 
 // producer/consumer blocks with the deferred-fold consumer (pc_sweep_lazy)
 template <class R, class Cost, int NT>
-__global__ void __launch_bounds__(128, 4) v2_lazy_pc_kernel(const EngineArgs a) {
+__global__ void __launch_bounds__(256, 2) v2_lazy_pc_kernel(const EngineArgs a) {
     v2_body<R, Cost, NT, false, false, true, true>(a);
 }
 
 // producer/consumer blocks for small chain counts: warp 0 consumes, warps
 // 1..3 produce (pc_sweep)
 template <class R, class Cost, int NT>
-__global__ void __launch_bounds__(128, 4) v2_pc_kernel(const EngineArgs a) {
+__global__ void __launch_bounds__(256, 2) v2_pc_kernel(const EngineArgs a) {
     v2_body<R, Cost, NT, false, false, true>(a);
 }
 
@@ -1121,7 +1121,7 @@ __device__ void pc_produce_x(PcEntryX<R, Cost::A>* buf, long long j0, int jn, in
 // folds only to settle and at level ends (engines.cpp:90-106 reads the
 // chain's energy there); v1_lazy_pc_kernel
 template <class R, class Cost, int NT, bool LZ = false>
-__global__ void __launch_bounds__(128, 4) v1_pc_kernel(const EngineArgs a) {
+__global__ void __launch_bounds__(256, 2) v1_pc_kernel(const EngineArgs a) {
     constexpr int A = Cost::A;
     fn_param_init<Cost>(a.fparam);
     extern __shared__ __align__(16) unsigned char smem_raw[];
