@@ -257,6 +257,7 @@ struct psa_plan {
     bool pc = false;              // producer/consumer blocks (v2_pc_kernel)
     bool lazy = false;            // deferred fold (v2_lazy_kernel)
     bool lazy_pc = false;         // producer/consumer with the deferred-fold consumer
+    bool v0 = false;              // the V0 latency kernel (v0_kernel)
     uint64_t last_settles = 0;    // exact-fold decisions of the last fetched run
     size_t mask_stride = 0;
     const void* kernel = nullptr; // the engine kernel this plan launches
@@ -454,6 +455,18 @@ void plan_build(psa_plan* p, const psa_objective* f, const psa_engine_config* cf
             }
         }
     }
+    // V0 (one chain of V1, run_sequential): the latency path when the family
+    // has the deferred fold and the chain fits one warp's registers
+    if (engine == 1 && p->chains_local == 1 && p->world == 1 && lazy_allowed && p->ks.v0z && n <= 32 &&
+        (mode.empty() || mode == "v0")) {
+        p->v0 = true;
+        p->pc = false;
+        p->pair = false;
+        p->hbm_rows = false;
+        p->block = B = 128;
+        p->smem = 0;
+        kern = p->ks.v0z;
+    }
     p->kernel = kern;
     cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(p->smem)),
@@ -538,7 +551,7 @@ void plan_build(psa_plan* p, const psa_objective* f, const psa_engine_config* cf
     a.world = p->world;
     a.rank = p->rank;
     a.spin_limit = 60ll * 2000000000ll; // ~60 s at 2 GHz
-    if (p->lazy || p->lazy_pc) {
+    if (p->lazy || p->lazy_pc || p->v0) {
         a.lazy_r = lazy_rr;
         const char* adapt = std::getenv("PSA_LAZY_ADAPT"); // 0: never fall back (tests)
         a.lazy_adapt = !(adapt && adapt[0] == '0');
@@ -1009,7 +1022,8 @@ psa_status psa_plan_describe(const psa_plan* p, char* buf, int32_t capacity) {
     return guarded([&] {
         if (!p || !buf || capacity < 1) fail(PSA_ERR_INVALID_ARGUMENT, "parsa_b200: null argument");
         std::ostringstream d;
-        const char* layout = p->engine == 1 ? (p->pc && p->lazy_pc ? "v1_lazy_pc_kernel (deferred-fold consumer, producer/consumer warps, 32 chains per block)"
+        const char* layout = p->engine == 1 ? (p->v0 ? "v0_kernel (one chain in one warp's registers, deferred fold, producer warps)"
+                                               : p->pc && p->lazy_pc ? "v1_lazy_pc_kernel (deferred-fold consumer, producer/consumer warps, 32 chains per block)"
                                                : p->pc         ? "v1_pc_kernel (producer/consumer warps, 32 chains per block)"
                                                : p->pair       ? "v1_pair_kernel (two chains per thread, shared-memory pair rows)"
                                                : p->hbm_rows ? "v1_kernel (HBM SoA rows)"

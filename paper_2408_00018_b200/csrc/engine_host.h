@@ -154,6 +154,7 @@ struct EngineKernels {
     const void* v2pz; // chain pairs (binary32), shared-memory pair rows
     const void* v2pcz; // producer/consumer blocks with the deferred-fold consumer
     const void* v1pcz; // V1 producer/consumer blocks with the deferred-fold consumer
+    const void* v0z;   // V0 latency path (one chain in one warp's registers, n <= 32)
     double (*lazy_radius)(int n, const double* lower, const double* upper);
     double (*lazy_alpha_of)(int n);
 };

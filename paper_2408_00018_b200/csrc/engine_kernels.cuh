@@ -1530,6 +1530,176 @@ __global__ void sweep_one(const EngineArgs a, double* x, R* row, double* energy,
 }
 
 // ---------------------------------------------------------------------------
+// V0 latency path: run_sequential (engines.cpp:125-129) — ONE chain through
+// the whole ladder, 114600 dependent trials for C1's ladder — for the affine
+// families at n <= 32.  The chain lives in the registers of the consumer
+// warp (lane k holds t_k and x_k); every lane runs the same scalar
+// decision, so there is no vote: a trial is a broadcast read of its
+// proposal, one shuffle for the replaced term, the deferred-fold interval
+// test, and a predicated register move on acceptance.  Exact folds (settles,
+// level ends) run in index order through shuffles.  Warps 1..3 produce the
+// proposals (three Philox draws and the term) 32 trials ahead into a
+// double-buffered ring.  Outputs are those of the V1 kernels (one block:
+// trace candidates, end state, xbest slot 0), finalized by v1_finalize.
+// ---------------------------------------------------------------------------
+template <class R, class Cost>
+__global__ void __launch_bounds__(128, 1) v0_kernel(const EngineArgs a) {
+    using Fam = typename Cost::Fam;
+    using L = LazyOf<Fam>;
+    static_assert(Cost::A == 1, "deferred fold: one accumulator");
+    __shared__ PcEntryX<R, 1> ring[2][32];
+    __shared__ double lower_s[32], width_s[32];
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int n = a.n; // <= 32 (plan_build)
+    const bool producer = tid >= 32;
+    Box box;
+    if (tid < n && !a.uniform_box) {
+        lower_s[tid] = a.lower[tid];
+        width_s[tid] = a.width[tid];
+    }
+    box.lower = lower_s;
+    box.width = width_s;
+    box.lo0 = a.lo0;
+    box.w0 = a.w0;
+    box.uniform = a.uniform_box != 0;
+    __syncthreads();
+    const uint32_t c = a.chain_begin;
+    const PhiloxChain pch = philox_chain(c, 0u, a.keys);
+    const uint32_t ctr0 = a.random_start ? static_cast<uint32_t>(n) : 0u;
+    const long long total = static_cast<long long>(a.levels) * a.N;
+    const int rounds = static_cast<int>((total + 31) / 32);
+    const double idx_scale = static_cast<double>(n) * 0x1.0p-53;
+    // proposals for trials [32 k, 32 k + jn): one per producer thread
+    auto produce = [&](int k) {
+        const long long j0 = 32ll * k;
+        const int jn = total - j0 < 32 ? static_cast<int>(total - j0) : 32;
+        const int jj = tid - 32;
+        if (jj < jn) {
+            const uint32_t ctr = ctr0 + 3u * static_cast<uint32_t>(j0 + jj);
+            const uint64_t m1 = draw_bits53_fast(ctr, pch, a.keys);
+            const uint64_t m2 = draw_bits53_fast(ctr + 1, pch, a.keys);
+            PcEntryX<R, 1> en;
+            en.p.m = draw_bits53_fast(ctr + 2, pch, a.keys);
+            en.p.d = min(static_cast<int>(static_cast<double>(m1) * idx_scale), n - 1);
+            en.x = box.point(en.p.d, bits_to_uniform(m2));
+            bool ok;
+            Cost::cache_common(static_cast<R>(en.x), en.p.d, n, en.p.t, ok);
+            if (!ok) Cost::cache(static_cast<R>(en.x), en.p.d, n, en.p.t);
+            ring[k & 1][jj] = en;
+        }
+    };
+    // the chain: lane k holds x_k and its term
+    double x = 0;
+    R t = 0;
+    if (!producer && lane < n) {
+        x = a.random_start ? random_start_coord(a, box, c, lane) : a.start[lane];
+        R tt[1];
+        Cost::cache(static_cast<R>(x), lane, n, tt);
+        t = tt[0];
+    }
+    // exact energy in index order, lane dsub's term replaced by tsub
+    auto fold_lanes = [&](R tsub, int dsub) {
+        R acc[1] = {Fam::init(0, n)};
+        for (int k = 0; k < n; ++k) {
+            R v = __shfl_sync(0xffffffffu, t, k);
+            if (k == dsub) v = tsub;
+            acc[0] = fold<R>(Fam::op(0), acc[0], v);
+        }
+        return Fam::finish(acc, n);
+    };
+    R E = 0;
+    if (!producer) E = fold_lanes(R(0), -1);
+    bool have = true;
+    double chain_best = static_cast<double>(E);
+    uint64_t settles = 0;
+    if (producer) produce(0);
+    __syncthreads();
+    int level = 0, in_level = 0;
+    double T = a.temps[0];
+    float k2 = metropolis_k2(T);
+    const R sa = L::sigma > 0 ? static_cast<R>(a.lazy_alpha) : -static_cast<R>(a.lazy_alpha);
+    const R rr = static_cast<R>(a.lazy_r);
+    for (int k = 0; k < rounds; ++k) {
+        const long long j0 = 32ll * k;
+        const int jn = total - j0 < 32 ? static_cast<int>(total - j0) : 32;
+        if (producer) {
+            if (k + 1 < rounds) produce(k + 1);
+        } else {
+            const PcEntryX<R, 1>* cur = ring[k & 1];
+            // trial j + 1's proposal, band and replaced term are read during
+            // trial j (the term as it is before trial j's move, fixed up
+            // below if trial j moves the same coordinate), so consecutive
+            // trials share no dependent chain but that select
+            PcEntryX<R, 1> en = cur[0];
+            MBand b = metropolis_band(en.p.m);
+            R to = __shfl_sync(0xffffffffu, t, en.p.d);
+            for (int j = 0; j < jn; ++j) {
+                const PcEntryX<R, 1> nx = cur[j + 1 < jn ? j + 1 : j];
+                const MBand nb = metropolis_band(nx.p.m);
+                R tnx = __shfl_sync(0xffffffffu, t, nx.p.d);
+                const R q = (en.p.t[0] - to) * sa;
+                const R hi = q + rr, lo = q - rr;
+                int r = ((hi <= R(0)) | (static_cast<float>(hi) * k2 < b.lo))
+                            ? 1
+                            : (((lo > R(0)) & (static_cast<float>(lo) * k2 > b.hi)) ? 0 : -1);
+                bool settled = false;
+                if (r < 0) { // warp-uniform: every lane computed the same r
+                    if (!have) {
+                        E = fold_lanes(R(0), -1);
+                        have = true;
+                    }
+                    const R et = fold_lanes(en.p.t[0], en.p.d);
+                    int v = metropolis_fast<R>(et, E, k2, b);
+                    if (v < 0) v = Accept<R>::exact(static_cast<double>(et) - static_cast<double>(E), T, en.p.m);
+                    if (v) E = et;
+                    r = v;
+                    settled = true;
+                    ++settles;
+                }
+                if (r) {
+                    if (lane == en.p.d) {
+                        t = en.p.t[0];
+                        x = en.x;
+                    }
+                    if (!settled) have = false;
+                    if (nx.p.d == en.p.d) tnx = en.p.t[0];
+                }
+                en = nx;
+                b = nb;
+                to = tnx;
+                if (++in_level == a.N) {
+                    // level end (engines.cpp:90-106): the exact energy
+                    if (!have) {
+                        E = fold_lanes(R(0), -1);
+                        have = true;
+                    }
+                    if (static_cast<double>(E) < chain_best) chain_best = static_cast<double>(E);
+                    if (lane == 0)
+                        a.trace_cand[static_cast<size_t>(level) * gridDim.x + blockIdx.x] =
+                            !is_nan(chain_best) ? Cand{chain_best, static_cast<int32_t>(c), 0} : empty_cand();
+                    in_level = 0;
+                    if (++level < a.levels) {
+                        T = a.temps[level];
+                        k2 = metropolis_k2(T);
+                    }
+                }
+            }
+        }
+        __syncthreads();
+    }
+    if (!producer) {
+        if (lane < n) a.xbest[lane] = x; // slot 0 (engines.cpp:110-116: the end state)
+        if (lane == 0) {
+            a.cand[blockIdx.x] = Cand{static_cast<double>(E), static_cast<int32_t>(c), 0};
+            atomicAdd(&a.out_scalars->evaluations, static_cast<unsigned long long>(1 + total));
+            atomicAdd(&a.out_scalars->rng_draws,
+                      static_cast<unsigned long long>(3 * total + (a.random_start ? n : 0)));
+            atomicAdd(&a.out_scalars->exact_settles, static_cast<unsigned long long>(settles));
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Host-side dispatch over (precision, family)
 // ---------------------------------------------------------------------------
 
@@ -1561,6 +1731,7 @@ struct KernelSet {
         k.v2gzu = nullptr;
         k.v2pcz = nullptr;
         k.v1pcz = nullptr;
+        k.v0z = nullptr;
         k.v2pz = nullptr;
         k.lazy_radius = nullptr;
         k.lazy_alpha_of = nullptr;
@@ -1571,6 +1742,7 @@ struct KernelSet {
             k.v2gzu = reinterpret_cast<const void*>(&v2_lazy_kernel<R, Cost, 0, true, true>);
             k.v2pcz = reinterpret_cast<const void*>(&v2_lazy_pc_kernel<R, Cost, NT>);
             k.v1pcz = reinterpret_cast<const void*>(&v1_pc_kernel<R, Cost, NT, true>);
+            k.v0z = reinterpret_cast<const void*>(&v0_kernel<R, Cost>);
             k.lazy_radius = &LazyCost<Cost>::radius;
             k.lazy_alpha_of = &LazyCost<Cost>::alpha;
             if constexpr (PairOf<Cost>::value) k.v2pz = reinterpret_cast<const void*>(&v2_lazy_pair_kernel<R, Cost, NT>);

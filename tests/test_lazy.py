@@ -187,3 +187,25 @@ def test_v1_and_v0_lazy_consumer_match_oracle(gpu_lib, monkeypatch, family, lo, 
         got = device_run(engine, prob, cfg)
         want = oracle_async(prob, cfg)
         assert not same_run(got, want), (engine, chains, same_run(got, want))
+
+
+@pytest.mark.parametrize("family,lo,hi", LAZY)
+@pytest.mark.parametrize("prec", [0, 1])
+def test_v0_latency_kernel_matches_oracle(gpu_lib, monkeypatch, family, lo, hi, prec):
+    """run_sequential (engines.cpp:125-129) on the V0 latency kernel: the
+    chain in one warp's registers, every decision the reference's, level-end
+    energies exact folds; n = 1 / 10 / 32, shared and random starts, a
+    non-uniform box and temperatures low enough to settle."""
+    monkeypatch.delenv("PSA_V2_MODE", raising=False)
+    from oracle_lib import oracle_async
+    rng = np.random.default_rng(5)
+    for dim, start, sched in ((10, 0, (20.0, 0.002, 0.8, 64)), (32, 1, (1e-3, 1e-7, 0.3, 100)), (1, 1, (5.0, 0.5, 0.5, 10))):
+        lo_v = np.full(dim, lo) - rng.uniform(0, 0.1, dim) * (hi - lo) * (start == 1)
+        prob = Problem(family, dim, lo_v, hi)
+        cfg = Config(1, sched, 23 + dim, prec, start)
+        got = device_run(0, prob, cfg)
+        want = oracle_async(prob, cfg)
+        assert not same_run(got, want), (dim, start, same_run(got, want))
+    f = psa.ObjectiveFunction("v0", "v0", 10, psa.BoxDomain([lo] * 10, [hi] * 10), family)
+    with psa.Plan(f, psa.EngineConfig(n_chains=1, schedule=psa.AnnealSchedule(5.0, 0.5, 0.5, 10)), engine=1) as p:
+        assert p.description.startswith("v0_kernel"), p.description
