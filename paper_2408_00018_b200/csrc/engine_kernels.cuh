@@ -1626,63 +1626,90 @@ __global__ void __launch_bounds__(128, 1) v0_kernel(const EngineArgs a) {
             if (k + 1 < rounds) produce(k + 1);
         } else {
             const PcEntryX<R, 1>* cur = ring[k & 1];
-            // trial j + 1's proposal, band and replaced term are read during
-            // trial j (the term as it is before trial j's move, fixed up
-            // below if trial j moves the same coordinate), so consecutive
-            // trials share no dependent chain but that select
-            PcEntryX<R, 1> en = cur[0];
-            MBand b = metropolis_band(en.p.m);
-            R to = __shfl_sync(0xffffffffu, t, en.p.d);
-            for (int j = 0; j < jn; ++j) {
-                const PcEntryX<R, 1> nx = cur[j + 1 < jn ? j + 1 : j];
-                const MBand nb = metropolis_band(nx.p.m);
-                R tnx = __shfl_sync(0xffffffffu, t, nx.p.d);
-                const R q = (en.p.t[0] - to) * sa;
+            // the interval decision (sweep_lazy): 1 accept, 0 reject, -1 settle
+            auto decide = [&](R tn, R to, const MBand& bb) {
+                const R q = (tn - to) * sa;
                 const R hi = q + rr, lo = q - rr;
-                int r = ((hi <= R(0)) | (static_cast<float>(hi) * k2 < b.lo))
-                            ? 1
-                            : (((lo > R(0)) & (static_cast<float>(lo) * k2 > b.hi)) ? 0 : -1);
+                return ((hi <= R(0)) | (static_cast<float>(hi) * k2 < bb.lo))
+                           ? 1
+                           : (((lo > R(0)) & (static_cast<float>(lo) * k2 > bb.hi)) ? 0 : -1);
+            };
+            auto level_end = [&]() { // engines.cpp:90-106: the exact level-end energy
+                if (!have) {
+                    E = fold_lanes(R(0), -1);
+                    have = true;
+                }
+                if (static_cast<double>(E) < chain_best) chain_best = static_cast<double>(E);
+                if (lane == 0)
+                    a.trace_cand[static_cast<size_t>(level) * gridDim.x + blockIdx.x] =
+                        !is_nan(chain_best) ? Cand{chain_best, static_cast<int32_t>(c), 0} : empty_cand();
+                in_level = 0;
+                if (++level < a.levels) {
+                    T = a.temps[level];
+                    k2 = metropolis_k2(T);
+                }
+            };
+            auto move = [&](const PcEntryX<R, 1>& en) {
+                if (lane == en.p.d) {
+                    t = en.p.t[0];
+                    x = en.x;
+                }
+            };
+            int j = 0;
+            while (j < jn) {
+                const PcEntryX<R, 1> e0 = cur[j];
+                const MBand b0 = metropolis_band(e0.p.m);
+                // two trials of one level at once: trial 1's decision is made
+                // both for the term before trial 0 and for trial 0's new term
+                // (same coordinate), then selected by trial 0's outcome — two
+                // independent chains of work instead of one dependent chain
+                if (j + 1 < jn && in_level + 2 <= a.N) {
+                    const PcEntryX<R, 1> e1 = cur[j + 1];
+                    const MBand b1 = metropolis_band(e1.p.m);
+                    const R t0 = __shfl_sync(0xffffffffu, t, e0.p.d);
+                    const R t1 = __shfl_sync(0xffffffffu, t, e1.p.d);
+                    const int r0 = decide(e0.p.t[0], t0, b0);
+                    const int r1a = decide(e1.p.t[0], t1, b1);
+                    const int r1b = decide(e1.p.t[0], e0.p.t[0], b1);
+                    const int r1 = (r0 == 1 && e1.p.d == e0.p.d) ? r1b : r1a;
+                    if ((r0 >= 0) & (r1 >= 0)) { // warp-uniform
+                        if (r0) {
+                            move(e0);
+                            have = false;
+                        }
+                        if (r1) {
+                            move(e1);
+                            have = false;
+                        }
+                        in_level += 2;
+                        if (in_level == a.N) level_end();
+                        j += 2;
+                        continue;
+                    }
+                }
+                // one trial, settling if needed
+                const R to = __shfl_sync(0xffffffffu, t, e0.p.d);
+                int r = decide(e0.p.t[0], to, b0);
                 bool settled = false;
                 if (r < 0) { // warp-uniform: every lane computed the same r
                     if (!have) {
                         E = fold_lanes(R(0), -1);
                         have = true;
                     }
-                    const R et = fold_lanes(en.p.t[0], en.p.d);
-                    int v = metropolis_fast<R>(et, E, k2, b);
-                    if (v < 0) v = Accept<R>::exact(static_cast<double>(et) - static_cast<double>(E), T, en.p.m);
+                    const R et = fold_lanes(e0.p.t[0], e0.p.d);
+                    int v = metropolis_fast<R>(et, E, k2, b0);
+                    if (v < 0) v = Accept<R>::exact(static_cast<double>(et) - static_cast<double>(E), T, e0.p.m);
                     if (v) E = et;
                     r = v;
                     settled = true;
                     ++settles;
                 }
                 if (r) {
-                    if (lane == en.p.d) {
-                        t = en.p.t[0];
-                        x = en.x;
-                    }
+                    move(e0);
                     if (!settled) have = false;
-                    if (nx.p.d == en.p.d) tnx = en.p.t[0];
                 }
-                en = nx;
-                b = nb;
-                to = tnx;
-                if (++in_level == a.N) {
-                    // level end (engines.cpp:90-106): the exact energy
-                    if (!have) {
-                        E = fold_lanes(R(0), -1);
-                        have = true;
-                    }
-                    if (static_cast<double>(E) < chain_best) chain_best = static_cast<double>(E);
-                    if (lane == 0)
-                        a.trace_cand[static_cast<size_t>(level) * gridDim.x + blockIdx.x] =
-                            !is_nan(chain_best) ? Cand{chain_best, static_cast<int32_t>(c), 0} : empty_cand();
-                    in_level = 0;
-                    if (++level < a.levels) {
-                        T = a.temps[level];
-                        k2 = metropolis_k2(T);
-                    }
-                }
+                if (++in_level == a.N) level_end();
+                ++j;
             }
         }
         __syncthreads();
