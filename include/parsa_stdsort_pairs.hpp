@@ -422,32 +422,8 @@ __device__ inline void warp_heap_sort(KeyId* v, int first, int last, double tie_
     if (last - first > 1) warp_sort_distinct(v, first, last);
 }
 
-// the smallest key that occurs at least twice INSIDE [first, last), among
-// the caller's list of keys tied somewhere in the array (nties < 0: no list
-// — every key may tie, -inf); +inf when no listed key occurs twice here
-__device__ inline double range_tie_min(const KeyId* v, int first, int last, const double* ties, int nties) {
-    if (nties < 0) return -__builtin_huge_val();
-    const int lane = threadIdx.x & 31;
-    double tm = __builtin_huge_val();
-    for (int q = 0; q < nties; ++q) {
-        const double K = ties[q];
-        int cnt = 0;
-        for (int base = first; base < last && cnt < 2; base += 32) {
-            const int i = base + lane;
-            cnt += __popc(__ballot_sync(0xffffffffu, i < last && v[i].key == K));
-        }
-        if (cnt >= 2 && K < tm) tm = K;
-    }
-    return tm;
-}
-
-// ties / nties: keys that occur more than once in the whole array (nties < 0:
-// unknown).  A range in which no key occurs twice ends up in sorted order
-// whatever the algorithm does inside it — its elements never leave it — so
-// it is sorted directly; a heap range stops popping once its last tied key
-// is out (warp_heap_sort).
 __device__ inline void warp_sort(KeyId* v, int m, int* ls, int* rs, WarpSortLists L,
-                                 const double* ties = nullptr, int nties = -1) {
+                                 double tie_min = -__builtin_huge_val()) {
     const int lane = threadIdx.x & 31;
     if (m <= PSA_SORT_THRESHOLD) {
         if (lane == 0) insertion_sort(v, 0, m);
@@ -467,13 +443,8 @@ __device__ inline void warp_sort(KeyId* v, int m, int* ls, int* rs, WarpSortList
         int nn = 0, ns = 0; // warp-uniform
         for (int r = 0; r < nc; ++r) {
             const int f = cur[3 * r], l = cur[3 * r + 1], d = cur[3 * r + 2];
-            const double tm = range_tie_min(v, f, l, ties, nties);
-            if (tm == __builtin_huge_val()) { // no tie inside: its sorted order
-                warp_sort_distinct(v, f, l);
-                continue;
-            }
             if (d == 0) {
-                warp_heap_sort(v, f, l, tm);
+                warp_heap_sort(v, f, l, tie_min);
                 continue;
             }
             if (lane == 0) median_to_first(v, f, f + 1, f + (l - f) / 2, l - 1);

@@ -298,33 +298,31 @@ __global__ void __launch_bounds__(512, 1) nm_kernel(const NMArgs a) {
         has_nan = 1; // A/B builds: always the one-thread sort
 #endif
         const bool any_nan = __syncthreads_or(has_nan);
-        // the values held by two vertices (at most 8 listed; more: -1, no
-        // list).  After replace_worst the first n keys are still in sorted
-        // order, so ties are adjacent pairs there or the new value against
-        // any of them; after a full rank sort (w < 0) no list is made
-        int nties = -1;
+        // tie_min: the smallest value held by two vertices.  After
+        // replace_worst the first n keys are still in sorted order, so ties
+        // are adjacent pairs there or the new value against any of them;
+        // after a full rank sort (w < 0) it is not computed (-inf: the warp
+        // sort's heap phase then pops everything)
+        double tie_min = -__builtin_huge_val();
         if (w >= 0 && !any_nan) {
-            if (tid == 0) ist[2] = 0;
-            __syncthreads();
+            double t = __builtin_huge_val();
             for (int p = tid; p < n; p += B) {
                 const double k = kp[p].key;
-                if (p + 1 < n && k == kp[p + 1].key) {
-                    const int q = atomicAdd(&ist[2], 1);
-                    if (q < 8) red[q] = k;
-                }
-                if (k == kp[n].key) {
-                    const int q = atomicAdd(&ist[2], 1);
-                    if (q < 8) red[q] = k;
-                }
+                if (p + 1 < n && k == kp[p + 1].key) t = fmin(t, k);
+                if (k == kp[n].key) t = fmin(t, k);
             }
+            for (int o = 16; o > 0; o >>= 1) t = fmin(t, __shfl_xor_sync(0xffffffffu, t, o));
+            if ((tid & 31) == 0) red[tid >> 5] = t;
             __syncthreads();
-            nties = ist[2] <= 8 ? ist[2] : -1;
+            t = __builtin_huge_val();
+            for (int i = 0; i < (B + 31) / 32; ++i) t = fmin(t, red[i]);
+            tie_min = t;
             __syncthreads();
         }
         if (any_nan || n + 1 <= PSA_SORT_THRESHOLD) {
             if (tid == 0) psa_sort::sort(kp, n + 1);
         } else if (tid < 32) {
-            psa_sort::warp_sort(kp, n + 1, rk, saved, wsl, red, nties);
+            psa_sort::warp_sort(kp, n + 1, rk, saved, wsl, tie_min);
         }
         __syncthreads();
         const int old_best = ord_s[0];

@@ -11,17 +11,13 @@
 #include <cmath>
 #include <vector>
 
-// the keys occurring more than once (at most 8; more: -1)
-static int ties_of(const std::vector<double>& k, int m, double* out) {
+// the smallest key occurring more than once (+inf: none)
+static double tie_min_of(const std::vector<double>& k, int m) {
     std::vector<double> s(k.begin(), k.begin() + m);
     std::sort(s.begin(), s.end());
-    int c = 0;
     for (int i = 0; i + 1 < m; ++i)
-        if (s[i] == s[i + 1] && (c == 0 || out[c - 1] != s[i])) {
-            if (c == 8) return -1;
-            out[c++] = s[i];
-        }
-    return c;
+        if (s[i] == s[i + 1]) return s[i];
+    return INFINITY;
 }
 
 #include "parsa_stdsort.h"
@@ -61,7 +57,7 @@ __global__ void heap_kernel(int m, int pf, long long* cyc) {
     if (lane == 0) { cyc[0] = t1 - t0; cyc[1] = t2 - t1; }
 }
 
-__global__ void sort_kernel(const double* keys, int m, int* out_ids, long long* cyc, const double* ties, int nties) {
+__global__ void sort_kernel(const double* keys, int m, int* out_ids, long long* cyc, double tie_min) {
     __shared__ psa_sort::KeyId kp[1024];
     __shared__ int ls[1024], rs[1024], lists[10 * 80];
     const int lane = threadIdx.x;
@@ -69,10 +65,7 @@ __global__ void sort_kernel(const double* keys, int m, int* out_ids, long long* 
     __syncwarp();
     const psa_sort::WarpSortLists L{lists, lists + 3 * 80, lists + 6 * 80};
     const long long t0 = clock64();
-    __shared__ double tl[8];
-    if (lane < 8 && nties > 0 && lane < nties) tl[lane] = ties[lane];
-    __syncwarp();
-    psa_sort::warp_sort(kp, m, ls, rs, L, tl, nties);
+    psa_sort::warp_sort(kp, m, ls, rs, L, tie_min);
     const long long t1 = clock64();
     for (int p = lane; p < m; p += 32) out_ids[p] = kp[p].id;
     if (lane == 0) *cyc = t1 - t0;
@@ -85,8 +78,6 @@ int main() {
     cudaMalloc(&dk, 1024 * sizeof(double));
     cudaMalloc(&di, 1024 * sizeof(int));
     cudaMalloc(&dc, sizeof(long long));
-    double* dt;
-    cudaMalloc(&dt, 8 * sizeof(double));
     srand(7);
     int bad = 0, cases = 0;
     std::vector<double> keys(1024);
@@ -102,10 +93,7 @@ int main() {
             for (int p = 0; p < m - 1; ++p) keys[p] = s[p].key;
         }
         cudaMemcpy(dk, keys.data(), m * sizeof(double), cudaMemcpyHostToDevice);
-        double tl[8];
-        const int nt = t % 2 ? ties_of(keys, m, tl) : -1;
-        cudaMemcpy(dt, tl, sizeof(tl), cudaMemcpyHostToDevice);
-        sort_kernel<<<1, 32>>>(dk, m, di, dc, dt, nt);
+        sort_kernel<<<1, 32>>>(dk, m, di, dc, t % 2 ? tie_min_of(keys, m) : -INFINITY);
         cudaMemcpy(got.data(), di, m * sizeof(int), cudaMemcpyDeviceToHost);
         std::vector<psa_sort::KeyId> want(m);
         for (int p = 0; p < m; ++p) want[p] = psa_sort::KeyId{keys[p], p, 0};
@@ -127,10 +115,7 @@ int main() {
                       : mode == 2 ? 1.0 : (p < m - 1 ? p / 5 : 50.0);
         }
         cudaMemcpy(dk, keys.data(), m * sizeof(double), cudaMemcpyHostToDevice);
-        double tl[8];
-        const int nt = ties_of(keys, m, tl);
-        cudaMemcpy(dt, tl, sizeof(tl), cudaMemcpyHostToDevice);
-        sort_kernel<<<1, 32>>>(dk, m, di, dc, dt, nt);
+        sort_kernel<<<1, 32>>>(dk, m, di, dc, tie_min_of(keys, m));
         long long c;
         cudaMemcpy(&c, dc, sizeof(c), cudaMemcpyDeviceToHost);
         std::printf("{\"input\": \"%s\", \"m\": 501, \"cycles\": %lld}\n", names[mode], c);
